@@ -1,0 +1,334 @@
+#!/usr/bin/env python3
+"""bench.py — PKT truss decomposition on B200 (BASELINE.json metric).
+
+A "step" = one full decomposition of the workload graph: edge-id map + degree
+orientation (build), support pass, device-resident level-synchronous peel, truss = s+2.
+
+  value : Medges/s with the CSR already resident in HBM (tdg_truss_device), whole job
+          over all ranks (replicas only: every rank decomposes its own copy; no data-path
+          collective — SURVEY §8(e)).
+  e2e   : the same through the host-pointer C-ABI call tdg_truss with pinned host
+          buffers: H2D of the CSR and D2H of truss[m] inside every timed step.
+  --impl reference : the reference's own CPU implementation (oracle/_ref, built from the
+          unmodified reference sources) on all host threads, on a bounded sample.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "truss decomposition Medges/s on 1 B200; achieved HBM GB/s vs peak"
+UNIT = "Medges/s"
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=int(os.environ.get("TDG_BENCH_CONFIG", "5")))
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ref-scale", type=int, default=18, help="RMAT scale of the bounded CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy test)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def cpu_sample(args):
+    """The bounded CPU sample: RMAT(--ref-scale, 16, seed 5) from the same generator family
+    as the workload (BASELINE config 5 is scale 25)."""
+    from paper_1707_02000_b200 import graphgen
+    n, m, off, nb = graphgen.rmat(args.ref_scale, 16, 5)
+    return n, m, off, nb
+
+
+def run_reference_cpu(args, steps: int, warmup: int):
+    """Time the reference's own path (build_truss_graph + truss_parallel, the CLI's
+    pipeline minus IO) on all host threads. Returns (median step s, samples, sample info)."""
+    from oracle import Csr, Reference
+    R = Reference()
+    n, m, off, nb = cpu_sample(args)
+    g = Csr(n, m, off, nb)
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    samples = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        d = R.truss_parallel(g, threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            samples.append((dt, d.times))
+    info = {"n": n, "m": m, "threads": threads,
+            "sample": f"RMAT scale {args.ref_scale} ef16 seed5 (same generator as C5 at 1/{2 ** (25 - args.ref_scale)} "
+                      f"of its vertices), m={m}; build_truss_graph+truss_parallel per step"}
+    return samples, info
+
+
+def bench_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    steps, warmup = max(1, args.steps), max(0, args.warmup)
+    samples, info = run_reference_cpu(args, steps, warmup)
+    per_step = [s for s, _ in samples]
+    t = float(np.median(per_step))
+    val = info["m"] / t / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": info["sample"], "n": info["n"], "m": info["m"]},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": info["threads"], "kind": "reference",
+                             "sample": info["sample"]},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "phases_s": {k: float(np.median([d[k] for _, d in samples])) for k in samples[0][1]}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+class ClockSampler:
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = [r for r in csv.reader(io.StringIO(out)) if len(r) == len(self.FIELDS)]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        reasons = set()
+        for r in rows:
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def bench_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_02000_b200 import graphgen, trussdec
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    # ---- workload (every rank builds the same seeded graph: replicas only)
+    pinned = {}
+
+    def alloc(n, m):
+        pinned["off"] = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+        pinned["nb"] = torch.empty(max(2 * m, 1), dtype=torch.int32, pin_memory=True)
+        return pinned["off"].numpy(), pinned["nb"].numpy()
+
+    t0 = time.time()
+    n, m, off_np, nb_np = graphgen.config(args.config, 0, alloc)
+    gen_s = time.time() - t0
+    off_h, nb_h = pinned["off"], pinned["nb"]
+    off_d = off_h.to(dev, non_blocking=True)
+    nb_d = nb_h.to(dev, non_blocking=True)
+    truss_d = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    truss_h = torch.empty(max(m, 1), dtype=torch.int32, pin_memory=True)
+    torch.cuda.synchronize()
+    in_bytes = (n + 1) * 8 + 2 * m * 4
+    flush = None if in_bytes > 2 * L2_BYTES else torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+
+    ctx = trussdec.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    nsl = np.zeros(n + 2, np.uint32)
+
+    def step_device():
+        return ctx.truss_device(n, m, off_d.data_ptr(), nb_d.data_ptr(), truss_d.data_ptr(), nsl)
+
+    for _ in range(max(args.warmup, 0)):
+        step_device()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    recs = []
+    for i in range(args.steps):
+        if flush is not None:
+            flush.fill_(i)
+        evs[i][0].record(stream)
+        _, t = step_device()
+        evs[i][1].record(stream)
+        recs.append(t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    value = world * m / (ms_per_step * 1e-3) / 1e6
+
+    truss = truss_d[:m].cpu().numpy().view(np.uint32)
+    tri = recs[-1]["triangles"]
+    sum_tau_m1 = int(truss.astype(np.uint64).sum()) - m if m else 0
+
+    # ---- e2e through the host-pointer C-ABI (pinned buffers; H2D + D2H inside each step)
+    e2e = None
+    if not args.no_e2e:
+        ctx.truss_host_ptrs(n, m, off_h.data_ptr(), nb_h.data_ptr(), truss_h.data_ptr(), nsl)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e_ms = []
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.truss_host_ptrs(n, m, off_h.data_ptr(), nb_h.data_ptr(), truss_h.data_ptr(), nsl)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        et = float(sum(e_ms))
+        if world > 1:
+            tt = torch.tensor([et], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            et = float(tt.item())
+        assert (truss_h[:m].numpy().view(np.uint32) == truss).all()
+        e2e = {"value": world * m / (et / args.steps * 1e-3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": 4 * m,
+               "ms_per_step": et / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline: algorithmic bytes over CUDA-event kernel time
+    st = ctx.stats(trussdec.CsrGraph(n, m, off_np, nb_np[: 2 * m]))
+    S1, S2 = st.deg_s1, st.sum_deg_sq
+    b_sup = 4 * S1 + 24 * m + 32 * tri
+    b_peel = 4 * S2 + 48 * tri + 55 * m + 5 * sum_tau_m1
+    avg = {k: float(np.mean([r[k] for r in recs])) for k in
+           ("build_ms", "support_ms", "peel_ms", "scan_ms", "process_ms", "total_ms")}
+    peak, peak_src = peaks()
+    kern = "peel" if avg["peel_ms"] >= avg["support_ms"] else "support"
+    k_ms = avg[kern + "_ms"]
+    k_bytes = b_peel if kern == "peel" else b_sup
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"C{args.config}", {}).get(kern)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": "k_peel (persistent cooperative level loop)" if kern == "peel"
+                else "k_support", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes": k_bytes,
+                "kernel_ms": k_ms,
+                "other": {"support": {"bytes": b_sup, "ms": avg["support_ms"],
+                                      "GBps": b_sup / (avg["support_ms"] * 1e-3) / 1e9},
+                          "peel": {"bytes": b_peel, "ms": avg["peel_ms"],
+                                   "GBps": b_peel / (avg["peel_ms"] * 1e-3) / 1e9}}}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            samples, info = run_reference_cpu(args, 1, 0)
+            tcpu = samples[0][0]
+            cpu = {"value": info["m"] / tcpu / 1e6, "unit": UNIT, "cores": info["threads"], "kind": "reference",
+                   "sample": info["sample"], "seconds": tcpu, "phases_s": samples[0][1]}
+        except Exception as e:  # the checker is optional on a box without oracle/_ref
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    from paper_1707_02000_b200 import graphgen as gg
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator, include/tdg_gen.h)",
+        "config": {"workload": gg.CONFIG_NAMES[args.config], "n": n, "m": m, "triangles": tri,
+                   "t_max": recs[-1]["t_max"], "sublevels": recs[-1]["sublevels"], "scans": recs[-1]["scans"],
+                   "parallelism": f"replicas x{world}", "l2": "inputs larger than L2" if flush is None
+                   else "L2 flushed between steps", "gen_s": gen_s},
+        "phases_ms": avg,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clocks,
+        "gpu_launches": int(sum(r["kernel_launches"] for r in recs)),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

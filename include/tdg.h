@@ -1,0 +1,145 @@
+/*
+ * tdg.h — C-ABI of the B200 (sm_100a) PKT truss-decomposition path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++/torch types. Each entry
+ * point replaces a reference function (paths relative to /root/reference/):
+ *
+ *   tdg_truss            <- trussdec::truss_parallel(const TrussGraph&, int)
+ *                           proj/include/trussdec/truss_parallel.hpp:72, impl
+ *                           proj/src/truss_parallel.cpp:106-150 (support pass + level-
+ *                           synchronous peel; truss[e] = final support + 2).
+ *   tdg_support          <- trussdec::support_am4(const TrussGraph&, int)
+ *                           proj/include/trussdec/triangle.hpp:16, proj/src/triangle.cpp:26-61
+ *   tdg_build_truss_graph<- trussdec::build_truss_graph(const CsrGraph&)
+ *                           proj/include/trussdec/graph.hpp:69, proj/src/graph.cpp:73-101
+ *   tdg_stats            <- trussdec::stats(const CsrGraph&)  proj/src/graph.cpp:135-150
+ *   tdg_scan             <- trussdec::scan(...)              truss_parallel.hpp:62, .cpp:21-37
+ *   tdg_process_sublevel <- trussdec::process_sublevel(...)  truss_parallel.hpp:67-68, .cpp:39-104
+ *
+ * Graph input (tdg_csr): undirected simple graph, adjacency lists sorted ascending,
+ * symmetric, no loops/duplicates (the reference's unchecked precondition,
+ * graph.hpp:19-20). n vertices, m undirected edges, offsets[n+1] (int64),
+ * neighbors[2m] (int32). Like the reference (graph.cpp:48-49) 2m must fit in uint32.
+ *
+ * Edge ids: the reference's — rank of (u,v), u<v, in ascending lexicographic order of the
+ * INPUT numbering (graph.cpp:86-99). Every per-edge output is indexed by it. The GPU
+ * orders work internally by degree but always scatters back to these ids.
+ *
+ * Pointers: the plain entry points take HOST pointers and copy in/out (timed as h2d/d2h);
+ * the *_device variants take DEVICE pointers (inputs already resident in HBM).
+ *
+ * Status: 0 = ok, < 0 = error; tdg_last_error() returns a thread-local message.
+ * Threading: a context owns one CUDA stream and its device buffers; calls on one
+ * context are serialised by the caller; distinct contexts are independent (reentrant).
+ * ctx == NULL selects a lazily created default context on the current device.
+ * There is no CPU fallback: without a usable sm_100 device every compute call fails.
+ */
+#ifndef TDG_H
+#define TDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TDG_OK 0
+#define TDG_ERR_INVALID (-1)   /* bad argument / contract violation (std::invalid_argument) */
+#define TDG_ERR_CUDA (-2)      /* CUDA runtime error or no usable device                  */
+#define TDG_ERR_NOMEM (-3)     /* device or pinned allocation failed (std::bad_alloc)    */
+#define TDG_ERR_RANGE (-4)     /* graph exceeds 32-bit edge width (graph.cpp:48-49)      */
+
+typedef struct tdg_context tdg_context;
+
+typedef struct tdg_csr {
+    int64_t n;
+    int64_t m;
+    const int64_t* offsets;   /* n+1 */
+    const int32_t* neighbors; /* 2m, each list sorted ascending */
+} tdg_csr;
+
+/* Phase timings (CUDA events on the context stream, milliseconds) and trace counters.
+ * support_ms/peel_ms mirror PhaseTimes{support, scan+processing}
+ * (truss_parallel.hpp:42-46). */
+typedef struct tdg_times {
+    double h2d_ms;      /* host -> device copy of the CSR (host-pointer entry points) */
+    double build_ms;    /* edge-id map + degree orientation (graph.cpp:73-101 equivalent) */
+    double support_ms;  /* support pass (triangle.cpp:26-61 equivalent)                  */
+    double peel_ms;     /* level loop: scans + sub-levels (truss_parallel.cpp:119-144)    */
+    double scan_ms;     /*   of which scan phases   (device clock, PhaseTimes::scan)       */
+    double process_ms;  /*   of which sub-levels    (device clock, PhaseTimes::processing) */
+    double d2h_ms;      /* device -> host copy of the per-edge result                     */
+    double total_ms;    /* whole call, device-side                                        */
+    uint64_t triangles; /* sum(support) / 3                                               */
+    uint64_t levels;    /* trace length = last non-empty level + 1                       */
+    uint64_t sublevels; /* sum(nsl)                                                       */
+    uint64_t scans;     /* scan passes actually executed (levels are skipped on device)   */
+    uint64_t compactions; /* adjacency compactions executed inside the peel               */
+    uint32_t t_max;     /* max trussness (0 when m == 0)                                  */
+    uint32_t kernel_launches; /* kernels this call launched                               */
+} tdg_times;
+
+typedef struct tdg_graph_stats {
+    uint64_t n, m, d_max;
+    uint64_t sum_deg_sq;      /* sum_v d(v)^2                 (graph.cpp:144)           */
+    uint64_t sum_dplus_sq;    /* sum_v d+(v)^2, natural order (graph.cpp:145-147)       */
+    uint64_t wedge_count;     /* (sum_deg_sq - 2m) / 2        (graph.cpp:148)           */
+    uint64_t deg_sum_dplus_sq;/* sum_u d+(u)^2 under the (degree, id) orientation       */
+    uint64_t deg_s1;          /* S1 = sum_{u->v} (d+(u) + d+(v)) under that orientation */
+} tdg_graph_stats;
+
+const char* tdg_version(void);
+const char* tdg_last_error(void);
+
+/* Context: one CUDA stream + grow-only device buffers on `device` (-1 = current device). */
+int tdg_context_create(int device, tdg_context** out);
+int tdg_context_destroy(tdg_context* ctx);
+/* Use an external CUDA stream (cudaStream_t as void*; NULL = the context's own). */
+int tdg_context_set_stream(tdg_context* ctx, void* stream);
+void* tdg_context_stream(tdg_context* ctx);
+/* Release cached device buffers (they are re-grown on the next call). */
+int tdg_context_trim(tdg_context* ctx);
+
+/* truss_parallel: truss_out[m] (host), nsl_out[min(nsl_cap, len)] (host) with
+ * *nsl_len = trace length; support_out[m] optional (initial supports, may be NULL);
+ * times optional. */
+int tdg_truss(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t* support_out,
+              uint32_t* nsl_out, uint64_t nsl_cap, uint64_t* nsl_len, tdg_times* times);
+/* Same with g->offsets / g->neighbors / truss_out / support_out in DEVICE memory
+ * (nsl_out stays a host array). Synchronises the stream before returning. */
+int tdg_truss_device(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out,
+                     uint32_t* support_out, uint32_t* nsl_out, uint64_t nsl_cap,
+                     uint64_t* nsl_len, tdg_times* times);
+
+/* support_am4: support_out[m] (host / device). */
+int tdg_support(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times);
+int tdg_support_device(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out,
+                       tdg_times* times);
+
+/* build_truss_graph: eo[n], eid[2m], el[2m] (el[2e], el[2e+1] = u < v). Host pointers. */
+int tdg_build_truss_graph(tdg_context* ctx, const tdg_csr* g, uint32_t* eo, uint32_t* eid,
+                          uint32_t* el);
+
+/* stats (host-pointer graph). */
+int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out);
+
+/* Step functions on caller-held frontier state (host arrays of length m, flags 0/1),
+ * for unit tests on hand-built states (tests/test_truss_parallel.cpp:25-105). They run
+ * the same device code as tdg_truss. scan: curr[*curr_size] = unprocessed edges with
+ * s == level, in_curr set. process_sublevel: drains curr (ownership rule, clamped
+ * decrements with repair), appends to next[*next_size] (in_next set), then marks curr
+ * processed and clears in_curr. The order inside curr/next is unspecified (as in the
+ * reference); compare as sets. */
+int tdg_scan(tdg_context* ctx, const uint32_t* s, uint64_t m, uint32_t level,
+             const uint8_t* processed, uint8_t* in_curr, uint32_t* curr, uint64_t* curr_size);
+int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32_t level,
+                         const uint32_t* curr, uint64_t curr_size, uint8_t* in_curr,
+                         uint8_t* in_next, uint8_t* processed, uint32_t* next,
+                         uint64_t* next_size);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TDG_H */

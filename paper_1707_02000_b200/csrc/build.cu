@@ -1,0 +1,194 @@
+// build.cu — edge-id map and degree orientation on the GPU.
+//
+// Reference: build_truss_graph, /root/reference/proj/src/graph.cpp:73-101. The reference
+// walks (u,v) pairs serially and finds mirror slots with a per-vertex cursor; here every
+// slot is independent:
+//   eo[u]   = first slot of u with neighbour > u                    (graph.cpp:80-84)
+//   P       = exclusive scan of up[u] = off[u+1]-eo[u]              (edge-id base per u)
+//   upper slot j of u (v>u): eid = P[u] + j - eo[u], el[eid] = (u,v)
+//   lower slot j of u (v<u): eid = P[v] + lower_bound(adj[eo[v]..off[v+1]), u)
+// Then the support pass's orientation (north-star item 1): u->v iff
+// (d(u),u) < (d(v),v); the oriented lists are order-preserving subsequences of adj,
+// compacted with one global scan of per-slot flags. All passes are slot-parallel
+// (load-balanced regardless of degree skew) and HBM-streaming except the lower-slot
+// binary search.
+
+#include <cub/device/device_scan.cuh>
+
+#include "tdg_kernels.h"
+
+namespace tdg {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(uint64_t items, int threads = kThreads) {
+    uint64_t b = (items + threads - 1) / threads;
+    if (b == 0) b = 1;
+    if (b > 0x7fffffffull) b = 0x7fffffffull;
+    return static_cast<unsigned>(b);
+}
+
+__global__ void k_off_to_u32(const int64_t* __restrict__ off64, uint32_t* __restrict__ off, uint32_t n1) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n1; i += uint64_t(gridDim.x) * blockDim.x)
+        off[i] = static_cast<uint32_t>(off64[i]);
+}
+
+// src[off[u]] = u for non-empty rows; a max-scan then fills every slot with its row.
+__global__ void k_row_start(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ src) {
+    uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n && off[u + 1] > off[u]) src[off[u]] = u;
+}
+
+__global__ void k_eo(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n,
+                     uint32_t* __restrict__ eo, uint32_t* __restrict__ up) {
+    uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) {
+        uint32_t o = off[u], d = off[u + 1] - o;
+        uint32_t e = o + upper_bound_u32(adj + o, d, u);
+        eo[u] = e;
+        up[u] = off[u + 1] - e;
+    } else if (u == n) {
+        up[n] = 0;
+    }
+}
+
+__global__ void k_eid(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                      const uint32_t* __restrict__ src, const uint32_t* __restrict__ eo,
+                      const uint32_t* __restrict__ P, uint64_t slots, uint32_t* __restrict__ eid,
+                      uint2* __restrict__ el, uint32_t* __restrict__ flag) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t u = src[j], v = adj[j];
+        uint32_t e;
+        if (v > u) {
+            e = P[u] + static_cast<uint32_t>(j - eo[u]);
+            el[e] = make_uint2(u, v);
+        } else {
+            const uint32_t lo = eo[v];
+            e = P[v] + lower_bound_u32(adj + lo, off[v + 1] - lo, u);
+        }
+        eid[j] = e;
+        if (flag) {
+            const uint32_t du = off[u + 1] - off[u], dv = off[v + 1] - off[v];
+            flag[j] = (du < dv || (du == dv && u < v)) ? 1u : 0u;
+        }
+    }
+}
+
+__global__ void k_orient(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ eid,
+                         const uint2* __restrict__ el, const uint32_t* __restrict__ flag,
+                         const uint32_t* __restrict__ pos, uint64_t slots, uint32_t* __restrict__ oadj,
+                         uint32_t* __restrict__ oeid, uint32_t* __restrict__ osrc) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        if (!flag[j]) continue;
+        const uint32_t t = pos[j], v = adj[j], e = eid[j];
+        const uint2 p = el[e];
+        oadj[t] = v;
+        oeid[t] = e;
+        osrc[t] = p.x ^ p.y ^ v;
+    }
+}
+
+__global__ void k_opos(const uint32_t* __restrict__ off, const uint32_t* __restrict__ pos, uint32_t n,
+                       uint32_t* __restrict__ opos) {
+    uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u <= n) opos[u] = pos[off[u]];
+}
+
+struct MaxOp {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+__global__ void k_stats(const uint32_t* __restrict__ off, const uint32_t* __restrict__ eo,
+                        const uint32_t* __restrict__ opos, uint32_t n, StatsAcc* acc) {
+    unsigned long long dmax = 0, sdd = 0, sdp = 0, sop = 0, s1 = 0;
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        unsigned long long d = off[u + 1] - off[u];
+        unsigned long long dpn = off[u + 1] - eo[u];
+        unsigned long long dp = opos[u + 1] - opos[u];
+        unsigned long long dm = d - dp;
+        dmax = d > dmax ? d : dmax;
+        sdd += d * d;
+        sdp += dpn * dpn;
+        sop += dp * dp;
+        s1 += dp * dp + dm * dp;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(kFull, dmax, o);
+        dmax = t > dmax ? t : dmax;
+        sdd += __shfl_xor_sync(kFull, sdd, o);
+        sdp += __shfl_xor_sync(kFull, sdp, o);
+        sop += __shfl_xor_sync(kFull, sop, o);
+        s1 += __shfl_xor_sync(kFull, s1, o);
+    }
+    if (lane_id() == 0) {
+        atomicMax(&acc->d_max, dmax);
+        atomicAdd(&acc->sum_deg_sq, sdd);
+        atomicAdd(&acc->sum_dplus_sq, sdp);
+        atomicAdd(&acc->deg_sum_dplus_sq, sop);
+        atomicAdd(&acc->deg_s1, s1);
+    }
+}
+
+}  // namespace
+
+size_t build_cub_bytes(uint32_t n, uint32_t m) {
+    size_t a = 0, b = 0, c = 0;
+    const uint64_t slots = 2ull * m;
+    cub::DeviceScan::InclusiveScan(nullptr, a, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                   MaxOp(), slots > 0 ? slots : 1);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                  static_cast<uint64_t>(n) + 1);
+    cub::DeviceScan::ExclusiveSum(nullptr, c, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                  slots + 1);
+    size_t r = a > b ? a : b;
+    return r > c ? r : c;
+}
+
+cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_orientation,
+                         cudaStream_t st, uint32_t* launches) {
+    const uint64_t slots = 2ull * m;
+    cudaError_t err;
+    size_t tmp = b.cub_bytes;
+    k_off_to_u32<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(b.off64, b.off, n + 1);
+    (*launches)++;
+    if (m == 0) return cudaGetLastError();
+    if ((err = cudaMemsetAsync(b.src, 0, slots * sizeof(uint32_t), st)) != cudaSuccess) return err;
+    k_row_start<<<grid_for(n), kThreads, 0, st>>>(b.off, n, b.src);
+    (*launches)++;
+    err = cub::DeviceScan::InclusiveScan(b.cub_tmp, tmp, b.src, b.src, MaxOp(), slots, st);
+    if (err != cudaSuccess) return err;
+    k_eo<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(b.off, b.adj, n, b.eo, b.up);
+    (*launches)++;
+    tmp = b.cub_bytes;
+    err = cub::DeviceScan::ExclusiveSum(b.cub_tmp, tmp, b.up, b.P, static_cast<uint64_t>(n) + 1, st);
+    if (err != cudaSuccess) return err;
+    const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
+    k_eid<<<gs, kThreads, 0, st>>>(b.off, b.adj, b.src, b.eo, b.P, slots, b.eid, b.el,
+                                   with_orientation ? b.flag : nullptr);
+    (*launches)++;
+    if (!with_orientation) return cudaGetLastError();
+    if ((err = cudaMemsetAsync(b.flag + slots, 0, sizeof(uint32_t), st)) != cudaSuccess) return err;
+    tmp = b.cub_bytes;
+    err = cub::DeviceScan::ExclusiveSum(b.cub_tmp, tmp, b.flag, b.pos, slots + 1, st);
+    if (err != cudaSuccess) return err;
+    k_orient<<<gs, kThreads, 0, st>>>(b.adj, b.eid, b.el, b.flag, b.pos, slots, b.oadj, b.oeid, b.osrc);
+    k_opos<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(b.off, b.pos, n, b.opos);
+    (*launches) += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats(const uint32_t* off, const uint32_t* eo, const uint32_t* opos, uint32_t n,
+                         StatsAcc* acc, cudaStream_t st, uint32_t* launches) {
+    cudaError_t err = cudaMemsetAsync(acc, 0, sizeof(StatsAcc), st);
+    if (err != cudaSuccess) return err;
+    unsigned g = grid_for(n) > 148u * 8u ? 148u * 8u : grid_for(n);
+    k_stats<<<g, kThreads, 0, st>>>(off, eo, opos, n, acc);
+    (*launches)++;
+    return cudaGetLastError();
+}
+
+}  // namespace tdg

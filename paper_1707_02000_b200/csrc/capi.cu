@@ -1,0 +1,559 @@
+// capi.cu — the extern "C" boundary (include/tdg.h): contexts, device buffers, H2D/D2H,
+// phase timing with CUDA events, error mapping. All compute is in build.cu / support.cu /
+// peel.cu; there is no host compute path.
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "tdg.h"
+#include "tdg_kernels.h"
+
+using namespace tdg;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Fail{e == cudaErrorMemoryAllocation ? TDG_ERR_NOMEM : TDG_ERR_CUDA,
+                    std::string(what) + ": " + cudaGetErrorString(e)};
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes, const char* name) {
+        if (bytes < 256) bytes = 256;
+        if (bytes <= cap) return;
+        release();
+        bytes = (bytes + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            throw Fail{TDG_ERR_NOMEM, std::string("device allocation of ") + name + " (" +
+                                          std::to_string(bytes >> 20) + " MiB) failed: " + cudaGetErrorString(e)};
+        }
+        cap = bytes;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct HostCtl {
+    PeelCtl peel;
+    SupportCtl sup;
+    StatsAcc stats;
+};
+
+}  // namespace
+
+struct tdg_context {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc;
+    DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2;
+    HostCtl* hctl = nullptr;
+    cudaEvent_t ev[8] = {};
+    uint32_t launches = 0;
+
+    void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+
+    void ensure_graph(uint64_t n, uint64_t m) {
+        const uint64_t slots = 2 * m;
+        off64.ensure((n + 1) * 8, "offsets64");
+        off.ensure((n + 1) * 4, "offsets");
+        adj.ensure(slots * 4, "adj");
+        src.ensure(slots * 4, "src");
+        eo.ensure(n * 4, "eo");
+        up.ensure((n + 1) * 4, "up");
+        P.ensure((n + 1) * 4, "P");
+        eid.ensure(slots * 4, "eid");
+        el.ensure(m * 8, "el");
+        flag.ensure((slots + 1) * 4, "flag");
+        pos.ensure((slots + 1) * 4, "pos");
+        opos.ensure((n + 1) * 4, "opos");
+        oadj.ensure(m * 4, "oadj");
+        oeid.ensure(m * 4, "oeid");
+        osrc.ensure(m * 4, "osrc");
+        dl.ensure(n * 4, "dl");
+        s.ensure(m * 4, "support");
+        ctl.ensure(sizeof(PeelCtl), "ctl");
+        sctl.ensure(sizeof(SupportCtl), "sctl");
+        sacc.ensure(sizeof(StatsAcc), "stats");
+        cub.ensure(build_cub_bytes(static_cast<uint32_t>(n), static_cast<uint32_t>(m)), "cub");
+    }
+    void ensure_peel(uint64_t n, uint64_t m) {
+        stamp.ensure(m * 4, "stamp");
+        L0.ensure(m * 4, "L0");
+        L1.ensure(m * 4, "L1");
+        A0.ensure(m * 4, "A0");
+        A1.ensure(m * 4, "A1");
+        nsl.ensure((n + 2) * 4, "nsl");
+    }
+
+    BuildBufs build_bufs(const int64_t* off64_dev) const {
+        BuildBufs b;
+        b.off64 = off64_dev;
+        b.off = off.as<uint32_t>();
+        b.adj = adj.as<uint32_t>();
+        b.src = src.as<uint32_t>();
+        b.eo = eo.as<uint32_t>();
+        b.up = up.as<uint32_t>();
+        b.P = P.as<uint32_t>();
+        b.eid = eid.as<uint32_t>();
+        b.el = el.as<uint2>();
+        b.flag = flag.as<uint32_t>();
+        b.pos = pos.as<uint32_t>();
+        b.opos = opos.as<uint32_t>();
+        b.oadj = oadj.as<uint32_t>();
+        b.oeid = oeid.as<uint32_t>();
+        b.osrc = osrc.as<uint32_t>();
+        b.cub_tmp = cub.p;
+        b.cub_bytes = cub.cap;
+        return b;
+    }
+    DevGraph dev_graph(uint32_t n, uint32_t m) const {
+        DevGraph g;
+        g.n = n;
+        g.m = m;
+        g.off = off.as<uint32_t>();
+        g.adj = adj.as<uint32_t>();
+        g.eid = eid.as<uint32_t>();
+        g.el = el.as<uint2>();
+        g.dl = dl.as<uint32_t>();
+        g.opos = opos.as<uint32_t>();
+        g.oadj = oadj.as<uint32_t>();
+        g.oeid = oeid.as<uint32_t>();
+        g.osrc = osrc.as<uint32_t>();
+        return g;
+    }
+    PeelBufs peel_bufs(uint32_t n) const {
+        PeelBufs p;
+        p.s = s.as<uint32_t>();
+        p.stamp = stamp.as<uint32_t>();
+        p.L[0] = L0.as<uint32_t>();
+        p.L[1] = L1.as<uint32_t>();
+        p.A[0] = A0.as<uint32_t>();
+        p.A[1] = A1.as<uint32_t>();
+        p.Q[0] = src.as<uint2>();   // build scratch, free once the graph is built
+        p.Q[1] = flag.as<uint2>();
+        p.ctl = ctl.as<PeelCtl>();
+        p.nsl = nsl.as<uint32_t>();
+        p.nsl_cap = n + 1;
+        return p;
+    }
+    void trim() {
+        DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
+                         &osrc, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
+                         &truss, &sup, &f0, &f1, &f2};
+        for (DevBuf* b : all) b->release();
+    }
+    float ms(int a, int b) const {
+        float t = 0;
+        cudaEventElapsedTime(&t, ev[a], ev[b]);
+        return t;
+    }
+};
+
+namespace {
+
+std::mutex g_default_mu;
+tdg_context* g_default = nullptr;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return TDG_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return TDG_ERR_NOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TDG_ERR_INVALID;
+    }
+}
+
+void create_ctx(int device, tdg_context** out) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw Fail{TDG_ERR_CUDA, "no CUDA device available (this library has no CPU path)"};
+    }
+    if (device == -1) ck(cudaGetDevice(&device), "cudaGetDevice");
+    if (device < 0 || device >= count) throw Fail{TDG_ERR_INVALID, "device index out of range"};
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        throw Fail{TDG_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (B200); kernels are built for sm_100a only"};
+    if (!prop.cooperativeLaunch) throw Fail{TDG_ERR_CUDA, "device lacks cooperative launch"};
+    auto* c = new tdg_context;
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own;
+    for (auto& ev : c->ev) ck(cudaEventCreate(&ev), "cudaEventCreate");
+    ck(cudaMallocHost(reinterpret_cast<void**>(&c->hctl), sizeof(HostCtl)), "cudaMallocHost");
+    *out = c;
+}
+
+tdg_context* resolve(tdg_context* ctx) {
+    if (ctx) return ctx;
+    std::lock_guard<std::mutex> lk(g_default_mu);
+    if (!g_default) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        create_ctx(dev, &g_default);
+    }
+    return g_default;
+}
+
+struct Dims {
+    uint32_t n, m;
+};
+
+Dims check_graph(const tdg_csr* g, bool host_ptrs) {
+    if (!g) throw Fail{TDG_ERR_INVALID, "graph is NULL"};
+    if (g->n < 0 || g->m < 0) throw Fail{TDG_ERR_INVALID, "negative n or m"};
+    if (static_cast<uint64_t>(g->n) >= 0xffffffffull)
+        throw Fail{TDG_ERR_RANGE, "graph exceeds 32-bit vertex id width"};
+    if (2 * static_cast<uint64_t>(g->m) > 0xffffffffull)
+        throw Fail{TDG_ERR_RANGE, "graph exceeds 32-bit edge width (2m too large)"};  // graph.cpp:48-49
+    if (!g->offsets || (g->m > 0 && !g->neighbors)) throw Fail{TDG_ERR_INVALID, "NULL CSR array"};
+    if (host_ptrs && (g->offsets[0] != 0 || g->offsets[g->n] != 2 * g->m))
+        throw Fail{TDG_ERR_INVALID, "offsets must start at 0 and end at 2m"};
+    return Dims{static_cast<uint32_t>(g->n), static_cast<uint32_t>(g->m)};
+}
+
+// Upload / alias the CSR and build eo/eid/el (+ orientation). Records ev[0], ev[1], ev[2].
+void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, bool orient) {
+    c->ensure_graph(d.n, d.m);
+    const int64_t* off64 = g->offsets;
+    ck(cudaEventRecord(c->ev[0], c->stream), "event");
+    if (host_ptrs) {
+        ck(cudaMemcpyAsync(c->off64.p, g->offsets, (size_t(d.n) + 1) * 8, cudaMemcpyHostToDevice, c->stream), "H2D offsets");
+        if (d.m)
+            ck(cudaMemcpyAsync(c->adj.p, g->neighbors, size_t(d.m) * 8, cudaMemcpyHostToDevice, c->stream), "H2D neighbors");
+        off64 = c->off64.as<int64_t>();
+    } else if (d.m) {
+        ck(cudaMemcpyAsync(c->adj.p, g->neighbors, size_t(d.m) * 8, cudaMemcpyDeviceToDevice, c->stream), "D2D neighbors");
+    }
+    ck(cudaEventRecord(c->ev[1], c->stream), "event");
+    ck(launch_build(c->build_bufs(off64), d.n, d.m, orient, c->stream, &c->launches), "build kernels");
+    ck(cudaEventRecord(c->ev[2], c->stream), "event");
+}
+
+void fill_times(tdg_times* t, tdg_context* c, bool host, bool peel) {
+    if (!t) return;
+    std::memset(t, 0, sizeof(*t));
+    t->h2d_ms = host ? c->ms(0, 1) : 0.0;
+    t->build_ms = c->ms(1, 2);
+    t->support_ms = c->ms(2, 3);
+    if (peel) {
+        t->peel_ms = c->ms(3, 6);
+        t->d2h_ms = host ? c->ms(4, 5) : 0.0;
+        t->total_ms = c->ms(0, 5);
+    } else {
+        t->d2h_ms = host ? c->ms(3, 5) : 0.0;
+        t->total_ms = c->ms(0, 5);
+    }
+    t->triangles = c->hctl->sup.tri3 / 3;
+    t->kernel_launches = c->launches;
+}
+
+int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t* support_out,
+               uint32_t* nsl_out, uint64_t nsl_cap, uint64_t* nsl_len, tdg_times* times, bool host) {
+    return guarded([&] {
+        if (!truss_out) throw Fail{TDG_ERR_INVALID, "truss_out is NULL"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, host);
+        c->launches = 0;
+        stage_and_build(c, g, d, host, true);
+        c->ensure_peel(d.n, d.m);
+        const DevGraph dg = c->dev_graph(d.n, d.m);
+        ck(launch_support(dg, c->s.as<uint32_t>(), c->src.as<uint2>(), c->sctl.as<SupportCtl>(), c->sms,
+                          c->stream, &c->launches), "support kernels");
+        uint32_t* sup_dev = nullptr;
+        if (support_out && d.m) {
+            if (host) { c->sup.ensure(size_t(d.m) * 4, "support copy"); sup_dev = c->sup.as<uint32_t>(); }
+            else sup_dev = support_out;
+            ck(cudaMemcpyAsync(sup_dev, c->s.p, size_t(d.m) * 4, cudaMemcpyDeviceToDevice, c->stream), "support copy");
+        }
+        ck(cudaEventRecord(c->ev[3], c->stream), "event");
+        const PeelBufs pb = c->peel_bufs(d.n);
+        ck(launch_peel(dg, pb, c->sms, c->stream, &c->launches), "peel kernel");
+        ck(cudaEventRecord(c->ev[6], c->stream), "event");
+        uint32_t* tdev = truss_out;
+        if (host) { c->truss.ensure(size_t(d.m) * 4, "truss"); tdev = c->truss.as<uint32_t>(); }
+        ck(launch_finalize(c->s.as<uint32_t>(), d.m, tdev, pb.ctl, c->stream, &c->launches), "finalize kernel");
+        ck(cudaEventRecord(c->ev[4], c->stream), "event");
+        if (host && d.m) {
+            ck(cudaMemcpyAsync(truss_out, tdev, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H truss");
+            if (sup_dev) ck(cudaMemcpyAsync(support_out, sup_dev, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H support");
+        }
+        ck(cudaEventRecord(c->ev[5], c->stream), "event");
+        ck(cudaMemcpyAsync(&c->hctl->peel, pb.ctl, sizeof(PeelCtl), cudaMemcpyDeviceToHost, c->stream), "D2H ctl");
+        ck(cudaMemcpyAsync(&c->hctl->sup, c->sctl.p, sizeof(SupportCtl), cudaMemcpyDeviceToHost, c->stream), "D2H sctl");
+        ck(cudaStreamSynchronize(c->stream), "decomposition");
+        const PeelCtl& pc = c->hctl->peel;
+        if (pc.overflow || c->hctl->sup.overflow)
+            throw Fail{TDG_ERR_RANGE, "work queue exceeded 32-bit piece counter"};
+        const uint64_t len = d.m ? pc.levels_len : 0;
+        if (nsl_len) *nsl_len = len;
+        if (nsl_out && len) {
+            const uint64_t k = len < nsl_cap ? len : nsl_cap;
+            if (k) ck(cudaMemcpy(nsl_out, pb.nsl, k * 4, cudaMemcpyDeviceToHost), "D2H nsl");
+        }
+        if (times) {
+            fill_times(times, c, host, true);
+            times->levels = len;
+            times->sublevels = pc.sublevels;
+            times->scans = pc.scans;
+            times->compactions = pc.compactions;
+            times->scan_ms = pc.scan_ns * 1e-6;
+            times->process_ms = pc.proc_ns * 1e-6;
+            times->t_max = d.m ? pc.t_max : 0;
+        }
+    });
+}
+
+int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times, bool host) {
+    return guarded([&] {
+        if (!support_out) throw Fail{TDG_ERR_INVALID, "support_out is NULL"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, host);
+        c->launches = 0;
+        stage_and_build(c, g, d, host, true);
+        const DevGraph dg = c->dev_graph(d.n, d.m);
+        uint32_t* sdev = host ? c->s.as<uint32_t>() : support_out;
+        ck(launch_support(dg, sdev, c->src.as<uint2>(), c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches),
+           "support kernels");
+        ck(cudaEventRecord(c->ev[3], c->stream), "event");
+        if (host && d.m)
+            ck(cudaMemcpyAsync(support_out, sdev, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H support");
+        ck(cudaEventRecord(c->ev[5], c->stream), "event");
+        ck(cudaMemcpyAsync(&c->hctl->sup, c->sctl.p, sizeof(SupportCtl), cudaMemcpyDeviceToHost, c->stream), "D2H sctl");
+        ck(cudaStreamSynchronize(c->stream), "support");
+        if (c->hctl->sup.overflow) throw Fail{TDG_ERR_RANGE, "work queue exceeded 32-bit piece counter"};
+        fill_times(times, c, host, false);
+    });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tdg_version(void) { return "tdg 0.1 (sm_100a)"; }
+const char* tdg_last_error(void) { return g_err.c_str(); }
+
+int tdg_context_create(int device, tdg_context** out) {
+    return guarded([&] {
+        if (!out) throw Fail{TDG_ERR_INVALID, "out is NULL"};
+        create_ctx(device, out);
+    });
+}
+
+int tdg_context_destroy(tdg_context* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        ctx->trim();
+        for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
+        if (ctx->own) cudaStreamDestroy(ctx->own);
+        if (ctx->hctl) cudaFreeHost(ctx->hctl);
+        {
+            std::lock_guard<std::mutex> lk(g_default_mu);
+            if (g_default == ctx) g_default = nullptr;
+        }
+        delete ctx;
+    });
+}
+
+int tdg_context_set_stream(tdg_context* ctx, void* stream) {
+    return guarded([&] {
+        tdg_context* c = resolve(ctx);
+        c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+    });
+}
+
+void* tdg_context_stream(tdg_context* ctx) {
+    tdg_context* c = nullptr;
+    if (guarded([&] { c = resolve(ctx); }) != TDG_OK) return nullptr;
+    return c->stream;
+}
+
+int tdg_context_trim(tdg_context* ctx) {
+    return guarded([&] {
+        tdg_context* c = resolve(ctx);
+        c->use();
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->trim();
+    });
+}
+
+int tdg_truss(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t* support_out,
+              uint32_t* nsl_out, uint64_t nsl_cap, uint64_t* nsl_len, tdg_times* times) {
+    return truss_impl(ctx, g, truss_out, support_out, nsl_out, nsl_cap, nsl_len, times, true);
+}
+
+int tdg_truss_device(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t* support_out,
+                     uint32_t* nsl_out, uint64_t nsl_cap, uint64_t* nsl_len, tdg_times* times) {
+    return truss_impl(ctx, g, truss_out, support_out, nsl_out, nsl_cap, nsl_len, times, false);
+}
+
+int tdg_support(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times) {
+    return support_impl(ctx, g, support_out, times, true);
+}
+
+int tdg_support_device(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times) {
+    return support_impl(ctx, g, support_out, times, false);
+}
+
+int tdg_build_truss_graph(tdg_context* ctx, const tdg_csr* g, uint32_t* eo, uint32_t* eid, uint32_t* el) {
+    return guarded([&] {
+        if (!eo || !eid || !el) throw Fail{TDG_ERR_INVALID, "NULL output array"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, true);
+        c->launches = 0;
+        stage_and_build(c, g, d, true, false);
+        if (d.n) ck(cudaMemcpyAsync(eo, c->eo.p, size_t(d.n) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H eo");
+        if (d.m) {
+            ck(cudaMemcpyAsync(eid, c->eid.p, size_t(d.m) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H eid");
+            ck(cudaMemcpyAsync(el, c->el.p, size_t(d.m) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H el");
+        }
+        ck(cudaStreamSynchronize(c->stream), "build");
+    });
+}
+
+int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out) {
+    return guarded([&] {
+        if (!out) throw Fail{TDG_ERR_INVALID, "out is NULL"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, true);
+        c->launches = 0;
+        stage_and_build(c, g, d, true, true);
+        std::memset(out, 0, sizeof(*out));
+        out->n = d.n;
+        out->m = d.m;
+        if (d.m == 0) return;
+        ck(launch_stats(c->off.as<uint32_t>(), c->eo.as<uint32_t>(), c->opos.as<uint32_t>(), d.n,
+                        c->sacc.as<StatsAcc>(), c->stream, &c->launches), "stats kernel");
+        ck(cudaMemcpyAsync(&c->hctl->stats, c->sacc.p, sizeof(StatsAcc), cudaMemcpyDeviceToHost, c->stream), "D2H stats");
+        ck(cudaStreamSynchronize(c->stream), "stats");
+        const StatsAcc& a = c->hctl->stats;
+        out->d_max = a.d_max;
+        out->sum_deg_sq = a.sum_deg_sq;
+        out->sum_dplus_sq = a.sum_dplus_sq;
+        out->wedge_count = (a.sum_deg_sq - 2ull * d.m) / 2;
+        out->deg_sum_dplus_sq = a.deg_sum_dplus_sq;
+        out->deg_s1 = a.deg_s1;
+    });
+}
+
+int tdg_scan(tdg_context* ctx, const uint32_t* s, uint64_t m, uint32_t level, const uint8_t* processed,
+             uint8_t* in_curr, uint32_t* curr, uint64_t* curr_size) {
+    return guarded([&] {
+        if (!curr_size || (m && (!s || !processed || !in_curr || !curr))) throw Fail{TDG_ERR_INVALID, "NULL argument"};
+        if (m > 0x7fffffffull) throw Fail{TDG_ERR_RANGE, "m too large"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        *curr_size = 0;
+        if (m == 0) return;
+        const uint32_t mm = static_cast<uint32_t>(m);
+        c->s.ensure(m * 4, "support");
+        c->ensure_peel(0, m);
+        c->ctl.ensure(sizeof(PeelCtl), "ctl");
+        c->src.ensure(m * 8, "queue");
+        c->flag.ensure(m * 8, "queue");
+        c->f0.ensure(m, "processed");
+        c->f1.ensure(m, "in_curr");
+        ck(cudaMemcpyAsync(c->s.p, s, m * 4, cudaMemcpyHostToDevice, c->stream), "H2D s");
+        ck(cudaMemcpyAsync(c->f0.p, processed, m, cudaMemcpyHostToDevice, c->stream), "H2D processed");
+        ck(cudaMemcpyAsync(c->f1.p, in_curr, m, cudaMemcpyHostToDevice, c->stream), "H2D in_curr");
+        ck(cudaMemsetAsync(c->ctl.p, 0, sizeof(PeelCtl), c->stream), "memset");
+        DevGraph dg;
+        dg.m = mm;
+        PeelBufs pb = c->peel_bufs(0);
+        ck(launch_step_scan(dg, pb, level, c->f0.as<uint8_t>(), c->f1.as<uint8_t>(), c->sms, c->stream), "scan");
+        ck(cudaMemcpyAsync(&c->hctl->peel, pb.ctl, sizeof(PeelCtl), cudaMemcpyDeviceToHost, c->stream), "D2H ctl");
+        ck(cudaMemcpyAsync(in_curr, c->f1.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H in_curr");
+        ck(cudaStreamSynchronize(c->stream), "scan");
+        const uint32_t cs = c->hctl->peel.ph[0].out_size;
+        if (cs) ck(cudaMemcpy(curr, pb.L[0], size_t(cs) * 4, cudaMemcpyDeviceToHost), "D2H curr");
+        *curr_size = cs;
+    });
+}
+
+int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32_t level, const uint32_t* curr,
+                         uint64_t curr_size, uint8_t* in_curr, uint8_t* in_next, uint8_t* processed,
+                         uint32_t* next, uint64_t* next_size) {
+    return guarded([&] {
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, true);
+        if (!next_size || (d.m && (!s || !in_curr || !in_next || !processed || !next)) || (curr_size && !curr))
+            throw Fail{TDG_ERR_INVALID, "NULL argument"};
+        if (curr_size > d.m) throw Fail{TDG_ERR_INVALID, "curr_size exceeds m"};
+        *next_size = 0;
+        c->launches = 0;
+        stage_and_build(c, g, d, true, false);
+        if (d.m == 0) { ck(cudaStreamSynchronize(c->stream), "sync"); return; }
+        c->ensure_peel(d.n, d.m);
+        c->f0.ensure(d.m, "processed");
+        c->f1.ensure(d.m, "in_curr");
+        c->f2.ensure(d.m, "in_next");
+        const size_t m = d.m;
+        ck(cudaMemcpyAsync(c->s.p, s, m * 4, cudaMemcpyHostToDevice, c->stream), "H2D s");
+        ck(cudaMemcpyAsync(c->f0.p, processed, m, cudaMemcpyHostToDevice, c->stream), "H2D processed");
+        ck(cudaMemcpyAsync(c->f1.p, in_curr, m, cudaMemcpyHostToDevice, c->stream), "H2D in_curr");
+        ck(cudaMemcpyAsync(c->f2.p, in_next, m, cudaMemcpyHostToDevice, c->stream), "H2D in_next");
+        if (curr_size) ck(cudaMemcpyAsync(c->L0.p, curr, curr_size * 4, cudaMemcpyHostToDevice, c->stream), "H2D curr");
+        ck(cudaMemsetAsync(c->ctl.p, 0, sizeof(PeelCtl), c->stream), "memset");
+        const DevGraph dg = c->dev_graph(d.n, d.m);
+        const PeelBufs pb = c->peel_bufs(d.n);
+        ck(launch_step_process(dg, pb, level, static_cast<uint32_t>(curr_size), c->f1.as<uint8_t>(),
+                               c->f2.as<uint8_t>(), c->f0.as<uint8_t>(), c->sms, c->stream), "process_sublevel");
+        ck(cudaMemcpyAsync(s, c->s.p, m * 4, cudaMemcpyDeviceToHost, c->stream), "D2H s");
+        ck(cudaMemcpyAsync(processed, c->f0.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H processed");
+        ck(cudaMemcpyAsync(in_curr, c->f1.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H in_curr");
+        ck(cudaMemcpyAsync(in_next, c->f2.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H in_next");
+        ck(cudaMemcpyAsync(&c->hctl->peel, pb.ctl, sizeof(PeelCtl), cudaMemcpyDeviceToHost, c->stream), "D2H ctl");
+        ck(cudaStreamSynchronize(c->stream), "process_sublevel");
+        if (c->hctl->peel.overflow) throw Fail{TDG_ERR_RANGE, "work queue exceeded 32-bit piece counter"};
+        const uint32_t ns = c->hctl->peel.ph[1].out_size;
+        if (ns) ck(cudaMemcpy(next, pb.L[1], size_t(ns) * 4, cudaMemcpyDeviceToHost), "D2H next");
+        *next_size = ns;
+    });
+}
+
+}  // extern "C"

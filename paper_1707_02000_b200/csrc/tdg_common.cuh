@@ -1,0 +1,143 @@
+// tdg_common.cuh — shared device helpers and device-side data layout of the B200 PKT path.
+//
+// Layout in HBM (all 32-bit; the reference is uint32 throughout, graph.hpp:10-11):
+//   off[n+1]   CSR offsets (narrowed from the int64 C-ABI input)
+//   adj[2m]    working copy of the sorted adjacency (compacted in place by the peel)
+//   eid[2m]    reference edge id of every adjacency slot        (graph.cpp:86-99)
+//   el[m]      uint2 (u,v), u<v, indexed by edge id             (graph.cpp:98)
+//   dl[n]      live length of each adjacency list (peel compaction)
+//   opos[n+1], oadj[m], oeid[m], osrc[m]
+//              degree-ordered orientation u->v iff (d(u),u) < (d(v),v), each list a
+//              sorted subsequence of adj (support pass only)
+//   s[m]       support, stamp[m] sub-level stamp (peel)
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tdg {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kNone = 0xffffffffu;
+// Load balancing: a task (edge) whose probe count exceeds kBigWork is split into
+// kPiece-item pieces served from a queue; smaller tasks are packed 32 per warp.
+constexpr uint32_t kBigWork = 256;
+constexpr uint32_t kPiece = 512;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// Relaxed gpu-scope accesses for words other SMs update inside the same launch
+// (supports under atomicSub, sub-level stamps). They bypass the non-coherent L1.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+
+// First index in [0,len) with a[i] >= x (len if none). Branch-free halving: every lane
+// of a warp runs ceil(log2(len)) steps, so a warp probing one list stays converged.
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* __restrict__ a, uint32_t len,
+                                                    uint32_t x) {
+    if (len == 0) return 0;
+    const uint32_t* base = a;
+    uint32_t n = len;
+    while (n > 1) {
+        uint32_t half = n >> 1;
+        base = (base[half] < x) ? base + half : base;
+        n -= half;
+    }
+    return static_cast<uint32_t>(base - a) + (*base < x);
+}
+
+// Same for the first index with a[i] > x.
+__device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t* __restrict__ a, uint32_t len,
+                                                    uint32_t x) {
+    if (len == 0) return 0;
+    const uint32_t* base = a;
+    uint32_t n = len;
+    while (n > 1) {
+        uint32_t half = n >> 1;
+        base = (base[half] <= x) ? base + half : base;
+        n -= half;
+    }
+    return static_cast<uint32_t>(base - a) + (*base <= x);
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(kFull, v, o);
+        if (lane_id() >= static_cast<uint32_t>(o)) v += t;
+    }
+    return v;
+}
+
+// Owner lane of flat item `item` given per-lane exclusive prefixes `excl` (monotone):
+// the largest lane L with excl_L <= item. All 32 lanes must call.
+__device__ __forceinline__ uint32_t warp_owner(uint32_t excl, uint32_t item) {
+    uint32_t lo = 0;
+#pragma unroll
+    for (uint32_t step = 16; step > 0; step >>= 1) {
+        uint32_t e = __shfl_sync(kFull, excl, lo + step);
+        if (e <= item) lo += step;
+    }
+    return lo;
+}
+
+// Warp-aggregated append (the GPU form of BufferedAppender, appender.hpp:12-40): one
+// atomicAdd per warp. All 32 lanes must call; returns the slot for lanes with `pred`.
+__device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
+    uint32_t mask = __ballot_sync(kFull, pred);
+    if (mask == 0) return 0;
+    uint32_t leader = __ffs(mask) - 1;
+    uint32_t base = 0;
+    if (lane_id() == leader) base = atomicAdd(counter, static_cast<uint32_t>(__popc(mask)));
+    base = __shfl_sync(kFull, base, leader);
+    return base + static_cast<uint32_t>(__popc(mask & lanemask_lt()));
+}
+
+// Piece queue push: one packed 64-bit atomic returns (entry index, first piece) so the
+// entries' piece bases are ascending in entry order. Returns false on 32-bit overflow.
+__device__ __forceinline__ bool queue_push(unsigned long long* ctr, uint2* q, uint32_t task,
+                                           uint32_t work) {
+    uint32_t pieces = (work + kPiece - 1) / kPiece;
+    unsigned long long old = atomicAdd(ctr, (1ull << 32) | pieces);
+    uint32_t idx = static_cast<uint32_t>(old >> 32);
+    uint32_t base = static_cast<uint32_t>(old);
+    q[idx] = make_uint2(task, base);
+    return static_cast<unsigned long long>(base) + pieces <= 0xffffffffull;
+}
+
+// Entry owning piece p: last q with q[.].y <= p.
+__device__ __forceinline__ uint32_t queue_find(const uint2* q, uint32_t nq, uint32_t p) {
+    uint32_t lo = 0, hi = nq;  // invariant: q[lo].y <= p
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (q[mid].y <= p) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+struct DevGraph {
+    uint32_t n = 0, m = 0;
+    const uint32_t* off = nullptr;
+    uint32_t* adj = nullptr;
+    uint32_t* eid = nullptr;
+    const uint2* el = nullptr;
+    uint32_t* dl = nullptr;
+    const uint32_t* opos = nullptr;
+    const uint32_t* oadj = nullptr;
+    const uint32_t* oeid = nullptr;
+    const uint32_t* osrc = nullptr;
+};
+
+}  // namespace tdg

@@ -1,0 +1,100 @@
+// tdg_kernels.h — host-side launchers for the sm_100a kernels (internal, C++).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tdg_common.cuh"
+
+namespace tdg {
+
+// ---- build (graph.cpp:73-101 equivalent + degree orientation) ----
+struct BuildBufs {
+    const int64_t* off64;  // device, n+1
+    uint32_t* off;         // n+1
+    uint32_t* adj;         // 2m
+    uint32_t* src;         // 2m scratch (row of each slot)
+    uint32_t* eo;          // n
+    uint32_t* up;          // n+1 scratch
+    uint32_t* P;           // n+1 edge-id base per vertex
+    uint32_t* eid;         // 2m
+    uint2* el;             // m
+    uint32_t* flag;        // 2m+1 scratch
+    uint32_t* pos;         // 2m+1 scratch
+    uint32_t* opos;        // n+1
+    uint32_t* oadj;        // m
+    uint32_t* oeid;        // m
+    uint32_t* osrc;        // m
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+size_t build_cub_bytes(uint32_t n, uint32_t m);
+// with_orientation=false stops after eo/eid/el (tdg_build_truss_graph, step functions).
+cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_orientation,
+                         cudaStream_t st, uint32_t* launches);
+
+struct StatsAcc {
+    unsigned long long d_max, sum_deg_sq, sum_dplus_sq, deg_sum_dplus_sq, deg_s1;
+};
+cudaError_t launch_stats(const uint32_t* off, const uint32_t* eo, const uint32_t* opos, uint32_t n,
+                         StatsAcc* acc, cudaStream_t st, uint32_t* launches);
+
+// ---- support (triangle.cpp:26-61 equivalent) ----
+struct SupportCtl {
+    unsigned long long big;  // packed (entries << 32 | pieces)
+    unsigned long long tri3; // sum of supports
+    uint32_t piece_head, batch_head, overflow, smax;
+};
+cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint2* queue, SupportCtl* ctl,
+                           int sm_count, cudaStream_t st, uint32_t* launches);
+
+// ---- peel (truss_parallel.cpp:21-150 equivalent) ----
+struct PhaseCtr {
+    unsigned long long big;  // packed queue counter for the NEXT phase's piece queue
+    uint32_t out_size;       // list appends (curr for a scan, next for a sub-level)
+    uint32_t alive_size;     // scan: surviving alive edges
+    uint32_t min_s;          // scan: min support over survivors (level skipping)
+    uint32_t piece_head;     // sub-level: dynamic piece cursor
+    uint32_t batch_head;     // sub-level / scan: dynamic batch cursor
+    uint32_t pad;
+};
+struct PeelCtl {
+    PhaseCtr ph[3];
+    uint32_t levels_len;   // last non-empty level + 1
+    uint32_t sublevels;
+    uint32_t scans;
+    uint32_t compactions;
+    uint32_t overflow;
+    uint32_t final_stamp;
+    uint32_t t_max;
+    uint32_t pad;
+    unsigned long long scan_ns;  // device-clock time in scan phases (leader thread)
+    unsigned long long proc_ns;  // device-clock time in sub-level phases
+};
+struct PeelBufs {
+    uint32_t* s;
+    uint32_t* stamp;
+    uint32_t* L[2];
+    uint32_t* A[2];
+    uint2* Q[2];
+    PeelCtl* ctl;
+    uint32_t* nsl;
+    uint32_t nsl_cap;
+};
+// Whole level loop in one persistent cooperative launch.
+cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cudaStream_t st,
+                        uint32_t* launches);
+// truss[e] = s[e] + 2 and t_max.
+cudaError_t launch_finalize(const uint32_t* s, uint32_t m, uint32_t* truss, PeelCtl* ctl,
+                            cudaStream_t st, uint32_t* launches);
+
+// Step functions (tdg_scan / tdg_process_sublevel) on reference-style flags.
+cudaError_t launch_step_scan(const DevGraph& g, const PeelBufs& p, uint32_t level,
+                             const uint8_t* processed, uint8_t* in_curr, int sm_count,
+                             cudaStream_t st);
+cudaError_t launch_step_process(const DevGraph& g, const PeelBufs& p, uint32_t level,
+                                uint32_t curr_size, uint8_t* in_curr, uint8_t* in_next,
+                                uint8_t* processed, int sm_count, cudaStream_t st);
+
+}  // namespace tdg

@@ -1,0 +1,88 @@
+// trussdec_gpu.cpp — non-template parts of the C++ shim (see trussdec_gpu.hpp).
+#include "trussdec_gpu.hpp"
+
+namespace trussdec_gpu {
+
+namespace {
+struct CtxHolder {
+    tdg_context* ctx = nullptr;
+    ~CtxHolder() {
+        if (ctx) tdg_context_destroy(ctx);
+    }
+};
+thread_local CtxHolder t_ctx;
+}  // namespace
+
+tdg_context* default_context() {
+    if (!t_ctx.ctx) check(tdg_context_create(-1, &t_ctx.ctx));  // -1: current device
+    return t_ctx.ctx;
+}
+
+void raise_status(int status) {
+    const std::string msg = tdg_last_error();
+    if (status == TDG_ERR_INVALID) throw std::invalid_argument(msg);
+    if (status == TDG_ERR_NOMEM) throw std::bad_alloc();
+    throw std::runtime_error(msg);
+}
+
+TrussGraph build_truss_graph(const CsrGraph& g) {
+    TrussGraph tg;
+    tg.csr = g;
+    tg.eid.assign(2ull * g.m, 0);
+    tg.el.resize(g.m);
+    tg.eo.resize(g.n);
+    std::vector<std::int64_t> off64;
+    const tdg_csr v = view(g, off64);
+    std::vector<std::uint32_t> el2(2ull * g.m + 1);
+    std::vector<std::uint32_t> eo(g.n + 1ull), eid(2ull * g.m + 1);
+    check(tdg_build_truss_graph(default_context(), &v, eo.data(), eid.data(), el2.data()));
+    for (std::uint32_t u = 0; u < g.n; u++) tg.eo[u] = eo[u];
+    for (std::uint64_t j = 0; j < 2ull * g.m; j++) tg.eid[j] = eid[j];
+    for (std::uint32_t e = 0; e < g.m; e++) tg.el[e] = {el2[2ull * e], el2[2ull * e + 1]};
+    return tg;
+}
+
+GraphStats stats(const CsrGraph& g) {
+    std::vector<std::int64_t> off64;
+    const tdg_csr v = view(g, off64);
+    tdg_graph_stats st{};
+    check(tdg_stats(default_context(), &v, &st));
+    GraphStats out;
+    out.n = static_cast<std::uint32_t>(st.n);
+    out.m = static_cast<std::uint32_t>(st.m);
+    out.d_max = static_cast<std::uint32_t>(st.d_max);
+    out.wedge_count = st.wedge_count;
+    out.sum_deg_sq = st.sum_deg_sq;
+    out.sum_dplus_sq = st.sum_dplus_sq;
+    return out;
+}
+
+SupportArray support_am4(const TrussGraph& tg, int workers) { return support_am4_as<SupportArray>(tg, workers); }
+
+ParallelDecomposition truss_parallel(const TrussGraph& tg, int workers) {
+    return truss_parallel_as<ParallelDecomposition>(tg, workers);
+}
+
+void scan(const SupportArray& s, std::uint32_t level, LevelFrontier& f, int /*workers*/) {
+    std::uint64_t cs = 0;
+    check(tdg_scan(default_context(), s.data(), s.size(), level, f.processed.data(), f.in_curr.data(),
+                   f.curr.data(), &cs));
+    f.curr_size.store(cs);
+}
+
+void process_sublevel(LevelFrontier& f, const TrussGraph& tg, SupportArray& s, std::uint32_t level,
+                      MarkScratchPool&, int /*workers*/) {
+    std::vector<std::int64_t> off64;
+    const tdg_csr v = view(tg.csr, off64);
+    std::uint64_t ns = 0;
+    // The reference appends to next after next_size entries already present (it is reset
+    // by the driver between sub-levels, truss_parallel.cpp:139); keep that contract.
+    const std::size_t base = f.next_size.load();
+    std::vector<std::uint32_t> out(tg.csr.m + 1ull);
+    check(tdg_process_sublevel(default_context(), &v, s.data(), level, f.curr.data(), f.curr_size.load(),
+                               f.in_curr.data(), f.in_next.data(), f.processed.data(), out.data(), &ns));
+    for (std::uint64_t i = 0; i < ns; i++) f.next[base + i] = out[i];
+    f.next_size.store(base + ns);
+}
+
+}  // namespace trussdec_gpu
