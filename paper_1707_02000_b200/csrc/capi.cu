@@ -71,7 +71,7 @@ struct tdg_context {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc;
-    DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2;
+    DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum;
     HostCtl* hctl = nullptr;
     cudaEvent_t ev[8] = {};
     uint32_t launches = 0;
@@ -109,6 +109,7 @@ struct tdg_context {
         A0.ensure(m * 4, "A0");
         A1.ensure(m * 4, "A1");
         nsl.ensure((n + 2) * 4, "nsl");
+        bsum.ensure(sizeof(unsigned long long) * kMaxChunks, "bsum");
     }
 
     BuildBufs build_bufs(const int64_t* off64_dev) const {
@@ -155,8 +156,8 @@ struct tdg_context {
         p.L[1] = L1.as<uint32_t>();
         p.A[0] = A0.as<uint32_t>();
         p.A[1] = A1.as<uint32_t>();
-        p.Q[0] = src.as<uint2>();   // build scratch, free once the graph is built
-        p.Q[1] = flag.as<uint2>();
+        p.wpre = src.as<unsigned long long>();  // build scratch (2m u32), free once built
+        p.bsum = bsum.as<unsigned long long>();
         p.ctl = ctl.as<PeelCtl>();
         p.nsl = nsl.as<uint32_t>();
         p.nsl_cap = n + 1;
@@ -165,7 +166,7 @@ struct tdg_context {
     void trim() {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
                          &osrc, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
-                         &truss, &sup, &f0, &f1, &f2};
+                         &truss, &sup, &f0, &f1, &f2, &bsum};
         for (DevBuf* b : all) b->release();
     }
     float ms(int a, int b) const {
@@ -493,8 +494,7 @@ int tdg_scan(tdg_context* ctx, const uint32_t* s, uint64_t m, uint32_t level, co
         c->s.ensure(m * 4, "support");
         c->ensure_peel(0, m);
         c->ctl.ensure(sizeof(PeelCtl), "ctl");
-        c->src.ensure(m * 8, "queue");
-        c->flag.ensure(m * 8, "queue");
+        c->src.ensure(m * 8, "wpre");
         c->f0.ensure(m, "processed");
         c->f1.ensure(m, "in_curr");
         ck(cudaMemcpyAsync(c->s.p, s, m * 4, cudaMemcpyHostToDevice, c->stream), "H2D s");

@@ -14,22 +14,25 @@
 // final support + 2. Sub-level sets (hence nsl) and results are therefore identical to
 // the reference for any schedule.
 //
-// B200 design differences:
-//  * Device-resident loop: all levels and sub-levels run inside one cooperative launch;
-//    a sub-level costs one grid barrier (the reference pays 2 OpenMP barriers + a fork).
+// B200 design:
+//  * Device-resident loop: every level and sub-level runs inside one cooperative launch;
+//    a sub-level is two grid-barrier phases (prep, process); a level adds one scan phase.
 //  * Flags -> stamps: stamp[e] = index of the sub-level in which e is (or was) curr.
 //    processed(e) <=> 0 < stamp < K, in_curr(e) <=> stamp == K, next <=> stamp == K+1.
 //    Entering next is the single stamp store by the appending thread, so the
 //    reference's epilogue pass over curr (:97-102) and the flag swaps vanish.
 //  * No dense X[n] mark array (MarkScratchPool, truss_parallel.hpp:55-59): N(u)∩N(v) is
 //    computed by walking the shorter live list and binary-searching the longer one.
+//  * Item-balanced sub-levels: prep computes each curr edge's probe count and a chunked
+//    prefix sum; process splits the sub-level's total probe count W into ~4 pieces per
+//    warp, pulled dynamically, so a sub-level's critical path is ~W/(#warps) probes no
+//    matter how skewed its edges are (hub-hub edges spread over many warps, tiny late
+//    sub-levels use as many warps as they have probes).
 //  * Level 0 needs no intersections: s[e1] >= #live triangles of e1, so s==0 edges have
 //    none (the reference still marks/scans their lists).
 //  * Levels with no edges are skipped: the scan that finds curr empty also returns the
 //    minimum live support, which is the next non-empty level. Each scan compacts the
 //    live-edge list, so later levels stream only survivors.
-//  * Load balance: edges with more than kBigWork probes are split into kPiece pieces in a
-//    queue built while the edge is appended; the rest are packed 32 per warp.
 
 #include <cooperative_groups.h>
 
@@ -43,6 +46,7 @@ namespace {
 
 constexpr int kPeelThreads = 256;
 constexpr int kScanItems = 8;
+constexpr int kWarps = kPeelThreads / 32;
 
 struct PTask {
     uint32_t e1;
@@ -62,7 +66,7 @@ __device__ __forceinline__ PTask ptask(const DevGraph& g, uint32_t e1) {
 }
 
 __device__ __forceinline__ void reset_ctr(PhaseCtr* c) {
-    c->big = 0;
+    c->work = 0;
     c->out_size = 0;
     c->alive_size = 0;
     c->min_s = 0xffffffffu;
@@ -102,30 +106,51 @@ __device__ __forceinline__ void peel_probe(const DevGraph& g, uint32_t* s, uint3
     out1 = try_dec(s, stamp, level, K, e1, eb, ea, sa == K);  // :87
 }
 
-__device__ __forceinline__ void classify_push(const DevGraph& g, uint32_t e, PhaseCtr* out, uint2* q,
-                                              PeelCtl* ctl) {
-    const PTask k = ptask(g, e);
-    if (k.la > kBigWork)
-        if (!queue_push(&out->big, q, e, k.la)) ctl->overflow = 1;
+// Append up to two targets per lane to next, one atomic per warp (appender.hpp:12-40).
+__device__ __forceinline__ void emit(uint32_t o0, uint32_t o1, PhaseCtr* out, uint32_t* next) {
+    const uint32_t p0 = warp_append(o0 != kNone, &out->out_size);
+    if (o0 != kNone) next[p0] = o0;
+    const uint32_t p1 = warp_append(o1 != kNone, &out->out_size);
+    if (o1 != kNone) next[p1] = o1;
 }
 
-// Append up to two targets per lane to next (warp-aggregated) and queue heavy ones.
-__device__ __forceinline__ void emit(const DevGraph& g, uint32_t o0, uint32_t o1, PhaseCtr* out,
-                                     uint32_t* next, uint2* qnext, PeelCtl* ctl) {
-    const uint32_t p0 = warp_append(o0 != kNone, &out->out_size);
-    if (o0 != kNone) { next[p0] = o0; classify_push(g, o0, out, qnext, ctl); }
-    const uint32_t p1 = warp_append(o1 != kNone, &out->out_size);
-    if (o1 != kNone) { next[p1] = o1; classify_push(g, o1, out, qnext, ctl); }
+__device__ __forceinline__ unsigned long long shfl64(unsigned long long v, uint32_t src) {
+    const uint32_t lo = __shfl_sync(kFull, static_cast<uint32_t>(v), src);
+    const uint32_t hi = __shfl_sync(kFull, static_cast<uint32_t>(v >> 32), src);
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+// Block-wide exclusive scan of a u64 per thread; returns the exclusive prefix and sets
+// `total`. All threads of the block must call.
+__device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long long v, unsigned long long& total) {
+    __shared__ unsigned long long sh[kWarps];
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = shfl64(x, lane >= static_cast<uint32_t>(o) ? lane - o : lane);
+        if (lane >= static_cast<uint32_t>(o)) x += t;
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    unsigned long long woff = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; w++) {
+        const unsigned long long t = sh[w];
+        if (w < static_cast<int>(wid)) woff += t;
+        tot += t;
+    }
+    __syncthreads();
+    total = tot;
+    return woff + x - v;
 }
 
 // scan (truss_parallel.cpp:21-37) over the live-edge list A: survivors with s==level
 // become curr (stamp K), the others are compacted into Aout and their minimum support is
 // reduced for level skipping. Block-aggregated appends: 2 atomics per 2048 edges.
-__device__ void phase_scan(const DevGraph& g, uint32_t* s, uint32_t* stamp, uint32_t level,
-                           uint32_t K, const uint32_t* Ain, uint32_t nA, bool implicit,
-                           uint32_t* Aout, uint32_t* curr, uint2* q, PhaseCtr* ph, PeelCtl* ctl,
-                           bool classify) {
-    __shared__ uint32_t sh_c[kPeelThreads / 32], sh_a[kPeelThreads / 32];
+__device__ void phase_scan(uint32_t* s, uint32_t* stamp, uint32_t level, uint32_t K, const uint32_t* Ain,
+                           uint32_t nA, bool implicit, uint32_t* Aout, uint32_t* curr, PhaseCtr* ph) {
+    __shared__ uint32_t sh_c[kWarps], sh_a[kWarps];
     __shared__ uint32_t sh_bc, sh_ba;
     const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
     const uint64_t tile = uint64_t(kPeelThreads) * kScanItems;
@@ -160,7 +185,7 @@ __device__ void phase_scan(const DevGraph& g, uint32_t* s, uint32_t* stamp, uint
         __syncthreads();
         if (tid == 0) {
             uint32_t rc = 0, ra = 0;
-            for (int w = 0; w < kPeelThreads / 32; w++) {
+            for (int w = 0; w < kWarps; w++) {
                 uint32_t c = sh_c[w], a = sh_a[w];
                 sh_c[w] = rc; sh_a[w] = ra;
                 rc += c; ra += a;
@@ -173,12 +198,8 @@ __device__ void phase_scan(const DevGraph& g, uint32_t* s, uint32_t* stamp, uint
 #pragma unroll
         for (int k = 0; k < kScanItems; k++) {
             const uint32_t f = (kind >> (2 * k)) & 3u;
-            if (f == 1u) {
-                curr[pc++] = es[k];
-                if (classify && level > 0) classify_push(g, es[k], ph, q, ctl);
-            } else if (f == 2u) {
-                Aout[pa++] = es[k];
-            }
+            if (f == 1u) curr[pc++] = es[k];
+            else if (f == 2u) Aout[pa++] = es[k];
         }
         __syncthreads();
     }
@@ -186,70 +207,118 @@ __device__ void phase_scan(const DevGraph& g, uint32_t* s, uint32_t* stamp, uint
     if (lane == 0 && local_min != 0xffffffffu) atomicMin(&ph->min_s, local_min);
 }
 
-// process_sublevel (truss_parallel.cpp:39-104) for curr[0..cs): heavy edges from the
-// piece queue first, then light edges 32 per warp, `grab` batches per dynamic grab.
-__device__ void phase_process(const DevGraph& g, uint32_t* s, uint32_t* stamp, uint32_t level,
-                              uint32_t K, const uint32_t* curr, uint32_t cs, const uint2* q,
-                              uint32_t nq, uint32_t npieces, PhaseCtr* ph, uint32_t* next,
-                              uint2* qnext, uint32_t grab, PeelCtl* ctl, bool l0_shortcut) {
+__device__ __forceinline__ uint32_t chunk_len(uint32_t cs, uint32_t nchunks) {
+    return (cs + nchunks - 1) / nchunks;
+}
+
+// Sub-level prep: block b owns curr chunk b; writes the chunk-local exclusive prefix of
+// probe counts (min live degree of the two endpoints) and the chunk total.
+__device__ void phase_prep(const DevGraph& g, const uint32_t* curr, uint32_t cs, unsigned long long* wpre,
+                           unsigned long long* bsum) {
+    const uint32_t CH = chunk_len(cs, gridDim.x);
+    const uint64_t lo = uint64_t(blockIdx.x) * CH;
+    const uint64_t hi = lo + CH < cs ? lo + CH : cs;
+    unsigned long long run = 0;
+    for (uint64_t t0 = lo; t0 < hi; t0 += kPeelThreads) {
+        const uint64_t i = t0 + threadIdx.x;
+        unsigned long long w = 0;
+        if (i < hi) w = ptask(g, curr[i]).la;
+        unsigned long long tot;
+        const unsigned long long ex = block_excl_scan64(w, tot);
+        if (i < hi) wpre[i] = run + ex;
+        run += tot;
+    }
+    if (threadIdx.x == 0) bsum[blockIdx.x] = run;
+}
+
+// process_sublevel (truss_parallel.cpp:39-104) for curr[0..cs): the W probe items are cut
+// into pieces of P items (P ~ W / (4 * #warps), >= 32), pulled by warps dynamically. A
+// warp walks its piece 32 items per step; lane k holds task i+k (the curr edges whose
+// items can fall in the 32-item window), and each lane finds its item's owner with a
+// 5-step shuffle search over the tasks' start offsets.
+__device__ void phase_process(const DevGraph& g, uint32_t* s, uint32_t* stamp, uint32_t level, uint32_t K,
+                              const uint32_t* curr, uint32_t cs, const unsigned long long* wpre,
+                              const unsigned long long* bsum, uint32_t nchunks, PhaseCtr* ph,
+                              uint32_t* next) {
+    __shared__ unsigned long long sboff[kMaxChunks + 1];
+    // chunk offsets (exclusive scan of bsum), redundantly per block
+    {
+        const uint32_t per = (nchunks + kPeelThreads - 1) / kPeelThreads;
+        const uint32_t c0 = threadIdx.x * per;
+        unsigned long long loc = 0;
+        for (uint32_t c = c0; c < c0 + per && c < nchunks; c++) loc += bsum[c];
+        unsigned long long tot;
+        unsigned long long run = block_excl_scan64(loc, tot);
+        for (uint32_t c = c0; c < c0 + per && c < nchunks; c++) {
+            sboff[c] = run;
+            run += bsum[c];
+        }
+        if (threadIdx.x == 0) sboff[nchunks] = tot;
+        __syncthreads();
+    }
+    const unsigned long long W = sboff[nchunks];
+    if (W == 0) return;
+    const uint32_t CH = chunk_len(cs, nchunks);
+    const uint32_t nwarps = (gridDim.x * kPeelThreads) >> 5;
+    unsigned long long P = (W + 4ull * nwarps - 1) / (4ull * nwarps);
+    P = (P + 31) & ~31ull;
+    if (P < 32) P = 32;
+    const unsigned long long npieces = (W + P - 1) / P;
     const uint32_t lane = lane_id();
+
     while (true) {
         uint32_t p = 0;
         if (lane == 0) p = atomicAdd(&ph->piece_head, 1u);
         p = __shfl_sync(kFull, p, 0);
         if (p >= npieces) break;
-        const uint2 qe = q[queue_find(q, nq, p)];
-        const PTask k = ptask(g, qe.x);
-        const uint32_t begin = (p - qe.y) * kPiece;
-        const uint32_t end = min(k.la, begin + kPiece);
-        for (uint32_t j0 = begin; j0 < end; j0 += 32) {
-            const uint32_t j = j0 + lane;
+        const unsigned long long x0 = p * P;
+        const unsigned long long x1 = x0 + P < W ? x0 + P : W;
+        // task containing x0: largest chunk c with sboff[c] <= x0, then largest i in chunk
+        uint32_t clo = 0, chi = nchunks;  // sboff[clo] <= x0 < sboff[chi]
+        while (chi - clo > 1) {
+            const uint32_t mid = (clo + chi) >> 1;
+            if (sboff[mid] <= x0) clo = mid; else chi = mid;
+        }
+        uint32_t ilo = clo * CH, ihi = min(cs, (clo + 1) * CH);
+        const unsigned long long rel = x0 - sboff[clo];
+        while (ihi - ilo > 1) {
+            const uint32_t mid = (ilo + ihi) >> 1;
+            if (wpre[mid] <= rel) ilo = mid; else ihi = mid;
+        }
+        uint32_t i = ilo;
+        // Lanes hold tasks i..i+31 (starts st); `end_held` = start of task i+32. A step
+        // covers the items of held tasks only, so any mix of task sizes is handled.
+        uint32_t held = kNone;
+        PTask k{0, 0, 0, 0, 0, 0};
+        unsigned long long st = ~0ull, end_held = ~0ull;
+        for (unsigned long long base = x0; base < x1;) {
+            if (held != i) {
+                const uint32_t t = i + lane;
+                if (t < cs) { k = ptask(g, curr[t]); st = sboff[t / CH] + wpre[t]; }
+                else { st = ~0ull; }
+                unsigned long long s32 = ~0ull;
+                if (lane == 31 && t + 1 < cs) s32 = sboff[(t + 1) / CH] + wpre[t + 1];
+                end_held = shfl64(s32, 31);
+                held = i;
+            }
+            const unsigned long long limit = x1 < end_held ? x1 : end_held;
+            const uint32_t relk = st <= base ? 0u : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
+            const uint32_t own = warp_owner(relk, lane);
+            const unsigned long long so = shfl64(st, own);
+            const uint32_t e1 = __shfl_sync(kFull, k.e1, own);
+            const uint32_t oa = __shfl_sync(kFull, k.oa, own);
+            const uint32_t ob = __shfl_sync(kFull, k.ob, own);
+            const uint32_t lb = __shfl_sync(kFull, k.lb, own);
+            const uint32_t bv = __shfl_sync(kFull, k.b, own);
+            const unsigned long long x = base + lane;
             uint32_t o0 = kNone, o1 = kNone;
-            if (j < end) peel_probe(g, s, stamp, level, K, k.e1, k.oa, k.ob, k.lb, k.b, j, o0, o1);
-            emit(g, o0, o1, ph, next, qnext, ctl);
+            if (x < limit) peel_probe(g, s, stamp, level, K, e1, oa, ob, lb, bv, static_cast<uint32_t>(x - so), o0, o1);
+            emit(o0, o1, ph, next);
+            const unsigned long long nb = base + 32 < limit ? base + 32 : limit;
+            i = (nb >= end_held) ? i + 32 : i + warp_owner(relk, static_cast<uint32_t>(nb - base));
+            base = nb;
         }
     }
-    if (l0_shortcut && level == 0) return;  // s[e1]==0 => no live triangle on e1
-    const uint32_t span = 32u * grab;
-    while (true) {
-        uint32_t b = 0;
-        if (lane == 0) b = atomicAdd(&ph->batch_head, 1u);
-        b = __shfl_sync(kFull, b, 0);
-        const uint64_t t0 = uint64_t(b) * span;
-        if (t0 >= cs) break;
-        for (uint32_t sub = 0; sub < grab; sub++) {
-            const uint64_t tb = t0 + uint64_t(sub) * 32;
-            if (tb >= cs) break;
-            const uint64_t i = tb + lane;
-            PTask k{0, 0, 0, 0, 0, 0};
-            uint32_t w = 0;
-            if (i < cs) {
-                k = ptask(g, curr[i]);
-                w = k.la <= kBigWork ? k.la : 0;
-            }
-            const uint32_t incl = warp_incl_scan(w);
-            const uint32_t excl = incl - w;
-            const uint32_t total = __shfl_sync(kFull, incl, 31);
-            for (uint32_t base = 0; base < total; base += 32) {
-                const uint32_t item = base + lane;
-                const uint32_t own = warp_owner(excl, item);
-                const uint32_t j = item - __shfl_sync(kFull, excl, own);
-                const uint32_t e1 = __shfl_sync(kFull, k.e1, own);
-                const uint32_t oa = __shfl_sync(kFull, k.oa, own);
-                const uint32_t ob = __shfl_sync(kFull, k.ob, own);
-                const uint32_t lb = __shfl_sync(kFull, k.lb, own);
-                const uint32_t bv = __shfl_sync(kFull, k.b, own);
-                uint32_t o0 = kNone, o1 = kNone;
-                if (item < total) peel_probe(g, s, stamp, level, K, e1, oa, ob, lb, bv, j, o0, o1);
-                emit(g, o0, o1, ph, next, qnext, ctl);
-            }
-        }
-    }
-}
-
-__device__ __forceinline__ uint32_t grab_for(uint32_t cs, uint32_t nwarps) {
-    uint32_t g = cs / (32u * 8u * (nwarps ? nwarps : 1u));
-    return g < 1 ? 1 : (g > 16 ? 16 : g);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -259,24 +328,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 __device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
-__device__ __forceinline__ unsigned long long vload64(const unsigned long long* p) {
-    return *reinterpret_cast<const volatile unsigned long long*>(p);
-}
 
 // The whole truss_parallel level loop (truss_parallel.cpp:119-144) in one launch.
 __global__ void __launch_bounds__(kPeelThreads) k_peel(DevGraph g, PeelBufs pb) {
     cg::grid_group grid = cg::this_grid();
     PeelCtl* ctl = pb.ctl;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0;
     bool implicit = true;
     unsigned long long t_prev = leader ? gtimer() : 0;
     while (true) {
         // ---- scan at `level` (one grid barrier)
         if (leader) { reset_ctr(&ctl->ph[(j + 1) % 3]); ctl->scans++; }
-        phase_scan(g, pb.s, pb.stamp, level, K, pb.A[ai], nA, implicit, pb.A[ai ^ 1], pb.L[li], pb.Q[li],
-                   &ctl->ph[j % 3], ctl, true);
+        phase_scan(pb.s, pb.stamp, level, K, pb.A[ai], nA, implicit, pb.A[ai ^ 1], pb.L[li], &ctl->ph[j % 3]);
         grid.sync();
         if (leader) { const unsigned long long t = gtimer(); ctl->scan_ns += t - t_prev; t_prev = t; }
         j++;
@@ -284,7 +348,6 @@ __global__ void __launch_bounds__(kPeelThreads) k_peel(DevGraph g, PeelBufs pb) 
         uint32_t cs = vload(&r->out_size);
         nA = vload(&r->alive_size);
         const uint32_t mins = vload(&r->min_s);
-        unsigned long long big = vload64(&r->big);
         ai ^= 1;
         implicit = false;
         if (cs == 0) {
@@ -292,24 +355,26 @@ __global__ void __launch_bounds__(kPeelThreads) k_peel(DevGraph g, PeelBufs pb) 
             level = mins;  // skip empty levels
             continue;
         }
-        // ---- sub-levels (one grid barrier each)
+        // ---- sub-levels: prep + process (two grid barriers each; level 0 one)
         while (true) {
             if (leader) {
-                reset_ctr(&ctl->ph[(j + 1) % 3]);
                 if (level < pb.nsl_cap) pb.nsl[level]++; else ctl->overflow = 1;
                 ctl->sublevels++;
                 ctl->levels_len = level + 1;
+                reset_ctr(&ctl->ph[(j + 1) % 3]);
             }
-            phase_process(g, pb.s, pb.stamp, level, K, pb.L[li], cs, pb.Q[li], static_cast<uint32_t>(big >> 32),
-                          static_cast<uint32_t>(big), &ctl->ph[j % 3], pb.L[li ^ 1], pb.Q[li ^ 1],
-                          grab_for(cs, nwarps), ctl, true);
+            if (level > 0) {  // level 0: s[e1] == 0 bounds its live triangles to none
+                phase_prep(g, pb.L[li], cs, pb.wpre, pb.bsum);
+                grid.sync();
+                phase_process(g, pb.s, pb.stamp, level, K, pb.L[li], cs, pb.wpre, pb.bsum, gridDim.x,
+                              &ctl->ph[j % 3], pb.L[li ^ 1]);
+            }
             grid.sync();
             if (leader) { const unsigned long long t = gtimer(); ctl->proc_ns += t - t_prev; t_prev = t; }
             j++;
             K++;
             r = &ctl->ph[(j - 1) % 3];
             cs = vload(&r->out_size);
-            big = vload64(&r->big);
             li ^= 1;
             if (cs == 0) break;
         }
@@ -345,9 +410,8 @@ __global__ void k_step_stamps(const uint8_t* __restrict__ processed, const uint8
     if (blockIdx.x == 0 && threadIdx.x < 3) reset_ctr(&ctl->ph[threadIdx.x]);
 }
 
-__global__ void k_step_scan(DevGraph g, PeelBufs pb, uint32_t level) {
-    phase_scan(g, pb.s, pb.stamp, level, 2, pb.A[0], g.m, true, pb.A[1], pb.L[0], pb.Q[0], &pb.ctl->ph[0], pb.ctl,
-               false);
+__global__ void __launch_bounds__(kPeelThreads) k_step_scan(PeelBufs pb, uint32_t m, uint32_t level) {
+    phase_scan(pb.s, pb.stamp, level, 2, pb.A[0], m, true, pb.A[1], pb.L[0], &pb.ctl->ph[0]);
 }
 
 __global__ void k_step_scan_flags(const uint32_t* __restrict__ curr, PeelCtl* ctl, uint8_t* in_curr) {
@@ -356,15 +420,14 @@ __global__ void k_step_scan_flags(const uint32_t* __restrict__ curr, PeelCtl* ct
         in_curr[curr[i]] = 1;
 }
 
-__global__ void k_step_classify(DevGraph g, PeelBufs pb, uint32_t cs) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cs; i += gridDim.x * blockDim.x)
-        classify_push(g, pb.L[0][i], &pb.ctl->ph[0], pb.Q[0], pb.ctl);
+__global__ void __launch_bounds__(kPeelThreads) k_step_prep(DevGraph g, PeelBufs pb, uint32_t cs) {
+    phase_prep(g, pb.L[0], cs, pb.wpre, pb.bsum);
 }
 
-__global__ void k_step_process(DevGraph g, PeelBufs pb, uint32_t cs, uint32_t level) {
-    const unsigned long long big = pb.ctl->ph[0].big;
-    phase_process(g, pb.s, pb.stamp, level, 2, pb.L[0], cs, pb.Q[0], static_cast<uint32_t>(big >> 32),
-                  static_cast<uint32_t>(big), &pb.ctl->ph[1], pb.L[1], pb.Q[1], 1, pb.ctl, false);
+// Hand-built states may break the level-0 invariant, so the step form always probes.
+__global__ void __launch_bounds__(kPeelThreads) k_step_process(DevGraph g, PeelBufs pb, uint32_t cs, uint32_t level,
+                                                               uint32_t nchunks) {
+    phase_process(g, pb.s, pb.stamp, level, 2, pb.L[0], cs, pb.wpre, pb.bsum, nchunks, &pb.ctl->ph[1], pb.L[1]);
 }
 
 // Epilogue (truss_parallel.cpp:97-102) + in_next flags for the appended edges.
@@ -392,11 +455,12 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel, kPeelThreads, 0);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-    dim3 grid(static_cast<unsigned>(sm_count * per_sm)), block(kPeelThreads);
+    unsigned blocks = static_cast<unsigned>(sm_count * per_sm);
+    if (blocks > kMaxChunks) blocks = kMaxChunks;
     DevGraph gg = g;
     PeelBufs pp = p;
     void* args[] = {&gg, &pp};
-    err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_peel), grid, block, args, 0, st);
+    err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_peel), dim3(blocks), dim3(kPeelThreads), args, 0, st);
     (*launches) += 2;
     return err;
 }
@@ -412,7 +476,7 @@ cudaError_t launch_finalize(const uint32_t* s, uint32_t m, uint32_t* truss, Peel
 cudaError_t launch_step_scan(const DevGraph& g, const PeelBufs& p, uint32_t level, const uint8_t* processed,
                              uint8_t* in_curr, int sm_count, cudaStream_t st) {
     k_step_stamps<<<sm_count * 2, 256, 0, st>>>(processed, nullptr, g.m, p.stamp, p.ctl);
-    k_step_scan<<<sm_count, kPeelThreads, 0, st>>>(g, p, level);
+    k_step_scan<<<sm_count, kPeelThreads, 0, st>>>(p, g.m, level);
     k_step_scan_flags<<<sm_count, 256, 0, st>>>(p.L[0], p.ctl, in_curr);
     return cudaGetLastError();
 }
@@ -420,10 +484,11 @@ cudaError_t launch_step_scan(const DevGraph& g, const PeelBufs& p, uint32_t leve
 cudaError_t launch_step_process(const DevGraph& g, const PeelBufs& p, uint32_t level, uint32_t curr_size,
                                 uint8_t* in_curr, uint8_t* in_next, uint8_t* processed, int sm_count,
                                 cudaStream_t st) {
+    const uint32_t nchunks = static_cast<uint32_t>(sm_count);
     k_peel_init<<<sm_count, 256, 0, st>>>(g.off, g.n, g.dl, p.ctl);
     k_step_stamps<<<sm_count * 2, 256, 0, st>>>(processed, in_curr, g.m, p.stamp, p.ctl);
-    k_step_classify<<<sm_count, 256, 0, st>>>(g, p, curr_size);
-    k_step_process<<<sm_count * 2, kPeelThreads, 0, st>>>(g, p, curr_size, level);
+    k_step_prep<<<nchunks, kPeelThreads, 0, st>>>(g, p, curr_size);
+    k_step_process<<<sm_count * 2, kPeelThreads, 0, st>>>(g, p, curr_size, level, nchunks);
     k_step_process_flags<<<sm_count, 256, 0, st>>>(p.L[0], curr_size, p.L[1], p.ctl, in_curr, in_next, processed);
     return cudaGetLastError();
 }

@@ -50,8 +50,9 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint2* queue, Support
                            int sm_count, cudaStream_t st, uint32_t* launches);
 
 // ---- peel (truss_parallel.cpp:21-150 equivalent) ----
+constexpr uint32_t kMaxChunks = 2048;  // max blocks of the peel grid (one work chunk each)
 struct PhaseCtr {
-    unsigned long long big;  // packed queue counter for the NEXT phase's piece queue
+    unsigned long long work; // sub-level: total probe items (informational)
     uint32_t out_size;       // list appends (curr for a scan, next for a sub-level)
     uint32_t alive_size;     // scan: surviving alive edges
     uint32_t min_s;          // scan: min support over survivors (level skipping)
@@ -77,7 +78,8 @@ struct PeelBufs {
     uint32_t* stamp;
     uint32_t* L[2];
     uint32_t* A[2];
-    uint2* Q[2];
+    unsigned long long* wpre;  // per curr position: exclusive work prefix inside its chunk
+    unsigned long long* bsum;  // per chunk (= block of the prep phase): total work
     PeelCtl* ctl;
     uint32_t* nsl;
     uint32_t nsl_cap;
