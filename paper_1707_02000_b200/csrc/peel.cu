@@ -321,6 +321,93 @@ __device__ void phase_process(const DevGraph& g, uint32_t* s, uint32_t* stamp, u
     }
 }
 
+// Adjacency compaction (between levels): drop processed edges (0 < stamp < K) from every
+// live list, in place and order-preserving, and shrink dl. Lists longer than kBigList are
+// compacted by a whole block (block scan per 1024-entry chunk), the rest by one warp
+// (ballot per 32 entries). Processed edges are skipped by every probe anyway (:85), so
+// this only removes work; triangle sets seen by the peel are unchanged.
+constexpr uint32_t kBigList = 2048;
+constexpr unsigned long long kCompactNum = 4, kCompactDen = 5;  // compact at <= 80% live
+
+__device__ __forceinline__ bool processed_stamp(uint32_t st, uint32_t K) { return st != 0 && st < K; }
+
+// Pass 1 (long lists). Must be separated from pass 2 by a grid barrier: pass 1 shrinks dl,
+// which would otherwise let pass 2 see a list being compacted as "short".
+__device__ void phase_compact_long(const DevGraph& g, const uint32_t* stamp, uint32_t K) {
+    __shared__ uint32_t sh_big[kPeelThreads], sh_nbig;
+    // 1) long lists: one block each (found per 256-vertex tile)
+    for (uint64_t u0 = uint64_t(blockIdx.x) * kPeelThreads; u0 < g.n; u0 += uint64_t(gridDim.x) * kPeelThreads) {
+        if (threadIdx.x == 0) sh_nbig = 0;
+        __syncthreads();
+        const uint64_t uu = u0 + threadIdx.x;
+        if (uu < g.n && g.dl[uu] > kBigList) sh_big[atomicAdd(&sh_nbig, 1u)] = static_cast<uint32_t>(uu);
+        __syncthreads();
+        const uint32_t nbig = sh_nbig;
+        for (uint32_t bi = 0; bi < nbig; bi++) {
+        const uint32_t u = sh_big[bi];
+        const uint32_t len = g.dl[u];
+        uint32_t* adj = g.adj + g.off[u];
+        uint32_t* eid = g.eid + g.off[u];
+        unsigned long long wp = 0;
+        for (uint32_t c = 0; c < len; c += kPeelThreads * 4) {
+            uint32_t a[4], e[4];
+            uint32_t keep = 0, cnt = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint32_t idx = c + threadIdx.x * 4 + q;  // 4 consecutive: order kept
+                a[q] = 0;
+                e[q] = 0;
+                if (idx < len) {
+                    a[q] = adj[idx];
+                    e[q] = eid[idx];
+                    if (!processed_stamp(ld_relaxed(&stamp[e[q]]), K)) { keep |= 1u << q; cnt++; }
+                }
+            }
+            unsigned long long tot;
+            unsigned long long pos = wp + block_excl_scan64(cnt, tot);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (keep & (1u << q)) { adj[pos] = a[q]; eid[pos] = e[q]; pos++; }
+            wp += tot;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) g.dl[u] = static_cast<uint32_t>(wp);
+        }
+        __syncthreads();
+    }
+}
+
+// Pass 2 (short lists): one warp each, ballot compaction in list order.
+__device__ void phase_compact_short(const DevGraph& g, const uint32_t* stamp, uint32_t K) {
+    const uint32_t lane = lane_id();
+    const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
+    for (uint32_t u = gw; u < g.n; u += nw) {
+        const uint32_t len = g.dl[u];
+        if (len == 0 || len > kBigList) continue;
+        uint32_t* adj = g.adj + g.off[u];
+        uint32_t* eid = g.eid + g.off[u];
+        uint32_t wp = 0;
+        for (uint32_t c = 0; c < len; c += 32) {
+            const uint32_t idx = c + lane;
+            uint32_t a = 0, e = 0;
+            bool keep = false;
+            if (idx < len) {
+                a = adj[idx];
+                e = eid[idx];
+                keep = !processed_stamp(ld_relaxed(&stamp[e]), K);
+            }
+            const uint32_t bal = __ballot_sync(kFull, keep);
+            if (keep) {
+                const uint32_t pos = wp + __popc(bal & lanemask_lt());
+                adj[pos] = a;
+                eid[pos] = e;
+            }
+            wp += __popc(bal);
+        }
+        if (lane == 0) g.dl[u] = wp;
+    }
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -334,7 +421,7 @@ __global__ void __launch_bounds__(kPeelThreads) k_peel(DevGraph g, PeelBufs pb) 
     cg::grid_group grid = cg::this_grid();
     PeelCtl* ctl = pb.ctl;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0;
+    uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m;
     bool implicit = true;
     unsigned long long t_prev = leader ? gtimer() : 0;
     while (true) {
@@ -354,6 +441,17 @@ __global__ void __launch_bounds__(kPeelThreads) k_peel(DevGraph g, PeelBufs pb) 
             if (nA == 0) break;
             level = mins;  // skip empty levels
             continue;
+        }
+        // ---- compaction once the live edge count fell below kCompactFrac of the last one
+        if (level > 0 && (static_cast<unsigned long long>(cs) + nA) * kCompactDen <
+                             static_cast<unsigned long long>(live_at_compact) * kCompactNum) {
+            if (leader) { reset_ctr(&ctl->ph[(j + 1) % 3]); ctl->compactions++; }
+            phase_compact_long(g, pb.stamp, K);
+            grid.sync();
+            phase_compact_short(g, pb.stamp, K);
+            grid.sync();
+            j++;
+            live_at_compact = cs + nA;
         }
         // ---- sub-levels: prep + process (two grid barriers each; level 0 one)
         while (true) {
