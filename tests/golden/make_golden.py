@@ -117,8 +117,9 @@ def configs(ids):
         n, m, off, nb = graphgen.config(c)
         g = Csr(n, m, off, nb)
         tg = time.time() - t0
-        d = R.truss_parallel(g, os.cpu_count() or 8)
-        sup = R.support_am4(g, os.cpu_count() or 8)
+        workers = int(os.environ.get("TDG_GOLDEN_WORKERS", os.cpu_count() or 8))
+        d = R.truss_parallel(g, workers)
+        sup = R.support_am4(g, workers)
         vals, cnt = np.unique(d.truss, return_counts=True)
         doc["configs"][str(c)] = {
             "name": graphgen.CONFIG_NAMES[c], "n": n, "m": m,
@@ -128,7 +129,7 @@ def configs(ids):
             "t_max": int(d.truss.max()), "kclass_sizes": {int(v): int(k) for v, k in zip(vals, cnt)},
             "triangles": int(sup.astype(np.uint64).sum() // 3),
             "sum_tau_minus_1": int(d.truss.astype(np.uint64).sum() - m),
-            "ref_times_s": d.times, "ref_workers": os.cpu_count(), "gen_s": tg,
+            "ref_times_s": d.times, "ref_workers": workers, "gen_s": tg,
         }
         json.dump(doc, open(path, "w"), indent=1)
         print(f"C{c}: n={n} m={m} t_max={int(d.truss.max())} sublevels={sum(d.nsl)} ({time.time()-t0:.1f}s)")
