@@ -61,6 +61,23 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def max_over_ranks(x: float, dev=None) -> float:
+    """Max of a per-rank scalar over all ranks (gloo on CPU, nccl on GPU); x if single rank."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=dev if dev is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_value(world: int, m: int, ms_per_step: float) -> float:
+    """Replicas only: every rank decomposes its own copy, so the job processes world*m edges
+    per step; the step time is the max over ranks."""
+    return world * m / (ms_per_step * 1e-3) / 1e6
+
+
 # ----------------------------------------------------------------------------- CPU arm
 def cpu_sample(args):
     """The bounded CPU sample: RMAT(--ref-scale, 16, seed 5) from the same generator family
@@ -219,13 +236,9 @@ def bench_ours(args):
         dist.barrier()
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = float(sum(step_ms))
-    if world > 1:
-        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+    total_ms = max_over_ranks(float(sum(step_ms)), dev)
     ms_per_step = total_ms / args.steps
-    value = world * m / (ms_per_step * 1e-3) / 1e6
+    value = whole_job_value(world, m, ms_per_step)
 
     truss = truss_d[:m].cpu().numpy().view(np.uint32)
     tri = recs[-1]["triangles"]
@@ -246,13 +259,9 @@ def bench_ours(args):
             b.record(stream)
             torch.cuda.synchronize()
             e_ms.append(a.elapsed_time(b))
-        et = float(sum(e_ms))
-        if world > 1:
-            tt = torch.tensor([et], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            et = float(tt.item())
+        et = max_over_ranks(float(sum(e_ms)), dev)
         assert (truss_h[:m].numpy().view(np.uint32) == truss).all()
-        e2e = {"value": world * m / (et / args.steps * 1e-3) / 1e6, "unit": UNIT,
+        e2e = {"value": whole_job_value(world, m, et / args.steps), "unit": UNIT,
                "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": 4 * m,
                "ms_per_step": et / args.steps}
 
