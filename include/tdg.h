@@ -76,6 +76,9 @@ typedef struct tdg_times {
     uint64_t sublevels; /* sum(nsl)                                                       */
     uint64_t scans;     /* scan passes actually executed (levels are skipped on device)   */
     uint64_t compactions; /* adjacency compactions executed inside the peel               */
+    uint64_t probes;    /* peel probe items (hash lookups) over all sub-levels            */
+    uint64_t hits;      /* peel triangle visits (0 unless TDG_COUNT_HITS=1 in the env)    */
+    uint64_t dead_probes; /* probes of already-processed slots (same diagnostic switch)   */
     uint32_t t_max;     /* max trussness (0 when m == 0)                                  */
     uint32_t kernel_launches; /* kernels this call launched                               */
 } tdg_times;

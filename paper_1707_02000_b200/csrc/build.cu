@@ -98,6 +98,39 @@ __global__ void k_opos(const uint32_t* __restrict__ off, const uint32_t* __restr
     if (u <= n) opos[u] = pos[off[u]];
 }
 
+// Hash-table sizes in units of 4 slots: power of two >= max(4, 2d).
+__global__ void k_hsize(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ hq) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) {
+        const uint32_t d = off[u + 1] - off[u];
+        uint32_t sz = 0;
+        if (d) {
+            sz = 4;
+            while (sz < 2 * d) sz <<= 1;
+        }
+        hq[u] = sz >> 2;
+    } else if (u == n) {
+        hq[n] = 0;
+    }
+}
+
+// Insert every slot (x -> y, eid) into x's table; the value carries the orientation bit.
+__global__ void k_hinsert(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                          const uint32_t* __restrict__ src, const uint32_t* __restrict__ eid,
+                          const uint32_t* __restrict__ hoff4, uint64_t slots, unsigned long long* __restrict__ htab) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t x = src[j], y = adj[j];
+        const uint32_t dx = off[x + 1] - off[x], dy = off[y + 1] - off[y];
+        const bool up = dx < dy || (dx == dy && x < y);
+        const unsigned long long entry = (static_cast<unsigned long long>(eid[j] | (up ? kHUp : 0u)) << 32) | y;
+        unsigned long long* tab = htab + 4ull * hoff4[x];
+        const uint32_t mask = 4u * (hoff4[x + 1] - hoff4[x]) - 1u;
+        uint32_t h = hmix(y) & mask;
+        while (atomicCAS(&tab[h], ~0ull, entry) != ~0ull) h = (h + 1) & mask;
+    }
+}
+
 struct MaxOp {
     __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
 };
@@ -178,6 +211,27 @@ cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_o
     k_orient<<<gs, kThreads, 0, st>>>(b.adj, b.eid, b.el, b.flag, b.pos, slots, b.oadj, b.oeid, b.osrc);
     k_opos<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(b.off, b.pos, n, b.opos);
     (*launches) += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_htab_sizes(const uint32_t* off, uint32_t n, uint32_t* hq, uint32_t* hoff4, void* cub_tmp,
+                              size_t cub_bytes, cudaStream_t st, uint32_t* launches) {
+    k_hsize<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(off, n, hq);
+    (*launches)++;
+    size_t tmp = cub_bytes;
+    return cub::DeviceScan::ExclusiveSum(cub_tmp, tmp, hq, hoff4, static_cast<uint64_t>(n) + 1, st);
+}
+
+cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, const uint32_t* eid,
+                             const uint32_t* hoff4, uint32_t m, unsigned long long* htab, uint64_t htab_slots,
+                             cudaStream_t st, uint32_t* launches) {
+    if (m == 0) return cudaSuccess;
+    cudaError_t err = cudaMemsetAsync(htab, 0xff, htab_slots * sizeof(unsigned long long), st);
+    if (err != cudaSuccess) return err;
+    const uint64_t slots = 2ull * m;
+    const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
+    k_hinsert<<<gs, kThreads, 0, st>>>(off, adj, src, eid, hoff4, slots, htab);
+    (*launches)++;
     return cudaGetLastError();
 }
 

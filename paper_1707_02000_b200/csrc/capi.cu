@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -61,6 +62,7 @@ struct HostCtl {
     PeelCtl peel;
     SupportCtl sup;
     StatsAcc stats;
+    uint32_t htab_quads;
 };
 
 }  // namespace
@@ -71,7 +73,7 @@ struct tdg_context {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc;
-    DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum;
+    DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab;
     HostCtl* hctl = nullptr;
     cudaEvent_t ev[8] = {};
     uint32_t launches = 0;
@@ -101,15 +103,15 @@ struct tdg_context {
         sctl.ensure(sizeof(SupportCtl), "sctl");
         sacc.ensure(sizeof(StatsAcc), "stats");
         cub.ensure(build_cub_bytes(static_cast<uint32_t>(n), static_cast<uint32_t>(m)), "cub");
+        bsum.ensure(sizeof(unsigned long long) * kMaxChunks, "bsum");
     }
     void ensure_peel(uint64_t n, uint64_t m) {
-        stamp.ensure(m * 4, "stamp");
+        stamp.ensure(m * 8, "edge state");
         L0.ensure(m * 4, "L0");
         L1.ensure(m * 4, "L1");
         A0.ensure(m * 4, "A0");
         A1.ensure(m * 4, "A1");
         nsl.ensure((n + 2) * 4, "nsl");
-        bsum.ensure(sizeof(unsigned long long) * kMaxChunks, "bsum");
     }
 
     BuildBufs build_bufs(const int64_t* off64_dev) const {
@@ -146,12 +148,14 @@ struct tdg_context {
         g.oadj = oadj.as<uint32_t>();
         g.oeid = oeid.as<uint32_t>();
         g.osrc = osrc.as<uint32_t>();
+        g.hoff4 = hoff4.as<uint32_t>();
+        g.htab = htab.as<unsigned long long>();
         return g;
     }
     PeelBufs peel_bufs(uint32_t n) const {
         PeelBufs p;
         p.s = s.as<uint32_t>();
-        p.stamp = stamp.as<uint32_t>();
+        p.ss = stamp.as<unsigned long long>();
         p.L[0] = L0.as<uint32_t>();
         p.L[1] = L1.as<uint32_t>();
         p.A[0] = A0.as<uint32_t>();
@@ -161,12 +165,14 @@ struct tdg_context {
         p.ctl = ctl.as<PeelCtl>();
         p.nsl = nsl.as<uint32_t>();
         p.nsl_cap = n + 1;
+        const char* ch = std::getenv("TDG_COUNT_HITS");
+        p.count_hits = (ch && ch[0] == '1') ? 1u : 0u;
         return p;
     }
     void trim() {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
                          &osrc, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
-                         &truss, &sup, &f0, &f1, &f2, &bsum};
+                         &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab};
         for (DevBuf* b : all) b->release();
     }
     float ms(int a, int b) const {
@@ -252,7 +258,7 @@ Dims check_graph(const tdg_csr* g, bool host_ptrs) {
 }
 
 // Upload / alias the CSR and build eo/eid/el (+ orientation). Records ev[0], ev[1], ev[2].
-void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, bool orient) {
+void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, bool orient, bool tables) {
     c->ensure_graph(d.n, d.m);
     const int64_t* off64 = g->offsets;
     ck(cudaEventRecord(c->ev[0], c->stream), "event");
@@ -266,6 +272,20 @@ void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, b
     }
     ck(cudaEventRecord(c->ev[1], c->stream), "event");
     ck(launch_build(c->build_bufs(off64), d.n, d.m, orient, c->stream, &c->launches), "build kernels");
+    if (tables) {
+        // neighbour -> edge-id hash tables; their total size is read back once to size htab
+        c->hoff4.ensure((size_t(d.n) + 1) * 4, "hoff4");
+        ck(launch_htab_sizes(c->off.as<uint32_t>(), d.n, c->up.as<uint32_t>(), c->hoff4.as<uint32_t>(), c->cub.p,
+                             c->cub.cap, c->stream, &c->launches), "hash sizes");
+        ck(cudaMemcpyAsync(&c->hctl->htab_quads, c->hoff4.as<uint32_t>() + d.n, 4, cudaMemcpyDeviceToHost, c->stream),
+           "D2H table size");
+        ck(cudaStreamSynchronize(c->stream), "table size");
+        const uint64_t slots = 4ull * c->hctl->htab_quads;
+        c->htab.ensure(slots * 8, "hash tables");
+        ck(launch_htab_fill(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->src.as<uint32_t>(), c->eid.as<uint32_t>(),
+                            c->hoff4.as<uint32_t>(), d.m, c->htab.as<unsigned long long>(), slots, c->stream,
+                            &c->launches), "hash fill");
+    }
     ck(cudaEventRecord(c->ev[2], c->stream), "event");
 }
 
@@ -295,11 +315,11 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         c->use();
         const Dims d = check_graph(g, host);
         c->launches = 0;
-        stage_and_build(c, g, d, host, true);
+        stage_and_build(c, g, d, host, true, true);
         c->ensure_peel(d.n, d.m);
         const DevGraph dg = c->dev_graph(d.n, d.m);
-        ck(launch_support(dg, c->s.as<uint32_t>(), c->src.as<uint2>(), c->sctl.as<SupportCtl>(), c->sms,
-                          c->stream, &c->launches), "support kernels");
+        ck(launch_support(dg, c->s.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
+                          c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
         uint32_t* sup_dev = nullptr;
         if (support_out && d.m) {
             if (host) { c->sup.ensure(size_t(d.m) * 4, "support copy"); sup_dev = c->sup.as<uint32_t>(); }
@@ -312,7 +332,7 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         ck(cudaEventRecord(c->ev[6], c->stream), "event");
         uint32_t* tdev = truss_out;
         if (host) { c->truss.ensure(size_t(d.m) * 4, "truss"); tdev = c->truss.as<uint32_t>(); }
-        ck(launch_finalize(c->s.as<uint32_t>(), d.m, tdev, pb.ctl, c->stream, &c->launches), "finalize kernel");
+        ck(launch_finalize(pb.ss, d.m, tdev, pb.ctl, c->stream, &c->launches), "finalize kernel");
         ck(cudaEventRecord(c->ev[4], c->stream), "event");
         if (host && d.m) {
             ck(cudaMemcpyAsync(truss_out, tdev, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H truss");
@@ -339,6 +359,9 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
             times->compactions = pc.compactions;
             times->scan_ms = pc.scan_ns * 1e-6;
             times->process_ms = pc.proc_ns * 1e-6;
+            times->probes = pc.probes;
+            times->hits = pc.hits;
+            times->dead_probes = pc.dead;
             times->t_max = d.m ? pc.t_max : 0;
         }
     });
@@ -351,11 +374,11 @@ int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_
         c->use();
         const Dims d = check_graph(g, host);
         c->launches = 0;
-        stage_and_build(c, g, d, host, true);
+        stage_and_build(c, g, d, host, true, true);
         const DevGraph dg = c->dev_graph(d.n, d.m);
         uint32_t* sdev = host ? c->s.as<uint32_t>() : support_out;
-        ck(launch_support(dg, sdev, c->src.as<uint2>(), c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches),
-           "support kernels");
+        ck(launch_support(dg, sdev, c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
+                          c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
         ck(cudaEventRecord(c->ev[3], c->stream), "event");
         if (host && d.m)
             ck(cudaMemcpyAsync(support_out, sdev, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H support");
@@ -445,7 +468,7 @@ int tdg_build_truss_graph(tdg_context* ctx, const tdg_csr* g, uint32_t* eo, uint
         c->use();
         const Dims d = check_graph(g, true);
         c->launches = 0;
-        stage_and_build(c, g, d, true, false);
+        stage_and_build(c, g, d, true, false, false);
         if (d.n) ck(cudaMemcpyAsync(eo, c->eo.p, size_t(d.n) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H eo");
         if (d.m) {
             ck(cudaMemcpyAsync(eid, c->eid.p, size_t(d.m) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H eid");
@@ -462,7 +485,7 @@ int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out) {
         c->use();
         const Dims d = check_graph(g, true);
         c->launches = 0;
-        stage_and_build(c, g, d, true, true);
+        stage_and_build(c, g, d, true, true, false);
         std::memset(out, 0, sizeof(*out));
         out->n = d.n;
         out->m = d.m;
@@ -495,6 +518,7 @@ int tdg_scan(tdg_context* ctx, const uint32_t* s, uint64_t m, uint32_t level, co
         c->ensure_peel(0, m);
         c->ctl.ensure(sizeof(PeelCtl), "ctl");
         c->src.ensure(m * 8, "wpre");
+        c->bsum.ensure(sizeof(unsigned long long) * kMaxChunks, "bsum");
         c->f0.ensure(m, "processed");
         c->f1.ensure(m, "in_curr");
         ck(cudaMemcpyAsync(c->s.p, s, m * 4, cudaMemcpyHostToDevice, c->stream), "H2D s");
@@ -526,7 +550,7 @@ int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32
         if (curr_size > d.m) throw Fail{TDG_ERR_INVALID, "curr_size exceeds m"};
         *next_size = 0;
         c->launches = 0;
-        stage_and_build(c, g, d, true, false);
+        stage_and_build(c, g, d, true, false, true);
         if (d.m == 0) { ck(cudaStreamSynchronize(c->stream), "sync"); return; }
         c->ensure_peel(d.n, d.m);
         c->f0.ensure(d.m, "processed");

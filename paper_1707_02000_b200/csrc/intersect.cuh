@@ -1,0 +1,194 @@
+// intersect.cuh — work-balanced, warp-cooperative probe engine shared by the support pass
+// (support.cu) and the peel's sub-levels (peel.cu).
+//
+// A "task" probes every element x of its list A = elems[oa .. oa+la) against the
+// neighbour -> edge-id hash table of one vertex (tdg_common.cuh: 1-2 dependent accesses
+// per probe instead of a log2(d)-step binary search). The tasks' la items are laid out on
+// one global axis by a chunked exclusive prefix sum (prep_items); process_items cuts the
+// axis into equal pieces pulled dynamically by warps, so skew in list lengths never leaves
+// a warp with a long tail. Inside a piece a warp walks 32-item windows over consecutive
+// tasks: lane k holds task i+k and each lane finds its item's owner with a 5-step shuffle
+// search. Policy (per caller) supplies `load(t)`, `elems`, `find(task, x)` (edge id of the
+// searched side or kNone) and `visit(active, hit, task, ja, e)`, which all 32 lanes call together
+// (so it may use warp collectives).
+#pragma once
+
+#include "tdg_common.cuh"
+
+namespace tdg {
+
+struct ITask {
+    uint32_t id;      // peel: e1 ; support: edge id of the oriented edge a->b
+    uint32_t oa, la;  // probe list
+    uint32_t ob, lb;  // searched vertex: its hash table (quad offset, slot mask)
+    uint32_t aux;     // peel: the searched vertex's id (it never occurs in its own table)
+};
+
+__device__ __forceinline__ ITask shfl_task(const ITask& k, uint32_t src) {
+    ITask r;
+    r.id = __shfl_sync(kFull, k.id, src);
+    r.oa = __shfl_sync(kFull, k.oa, src);
+    r.la = __shfl_sync(kFull, k.la, src);
+    r.ob = __shfl_sync(kFull, k.ob, src);
+    r.lb = __shfl_sync(kFull, k.lb, src);
+    r.aux = __shfl_sync(kFull, k.aux, src);
+    return r;
+}
+
+__device__ __forceinline__ unsigned long long shfl64(unsigned long long v, uint32_t src) {
+    const uint32_t lo = __shfl_sync(kFull, static_cast<uint32_t>(v), src);
+    const uint32_t hi = __shfl_sync(kFull, static_cast<uint32_t>(v >> 32), src);
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+// Largest lane t with held_t <= key (held non-decreasing over lanes); 0 if none.
+__device__ __forceinline__ uint32_t warp_search_le(uint32_t held, uint32_t key) {
+    uint32_t lo = 0;
+#pragma unroll
+    for (uint32_t step = 16; step > 0; step >>= 1) {
+        const uint32_t v = __shfl_sync(kFull, held, lo + step);
+        if (v <= key) lo += step;
+    }
+    return lo;
+}
+
+template <int kThreads>
+__device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long long v, unsigned long long& total) {
+    constexpr int kW = kThreads / 32;
+    __shared__ unsigned long long sh[kW];
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = shfl64(x, lane >= static_cast<uint32_t>(o) ? lane - o : lane);
+        if (lane >= static_cast<uint32_t>(o)) x += t;
+    }
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    unsigned long long woff = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kW; w++) {
+        const unsigned long long t = sh[w];
+        if (w < static_cast<int>(wid)) woff += t;
+        tot += t;
+    }
+    __syncthreads();
+    total = tot;
+    return woff + x - v;
+}
+
+__device__ __forceinline__ uint32_t chunk_len(uint32_t ntasks, uint32_t nchunks) {
+    return (ntasks + nchunks - 1) / nchunks;
+}
+
+// Block b of a gridDim.x-block grid owns task chunk b: writes the chunk-local exclusive
+// prefix of the tasks' work (probe counts) and the chunk total bsum[b].
+template <int kThreads, class WorkF>
+__device__ void prep_items(uint32_t ntasks, WorkF&& work, unsigned long long* wpre, unsigned long long* bsum) {
+    const uint32_t CH = chunk_len(ntasks, gridDim.x);
+    const uint64_t lo = uint64_t(blockIdx.x) * CH;
+    const uint64_t hi = lo + CH < ntasks ? lo + CH : ntasks;
+    unsigned long long run = 0;
+    for (uint64_t t0 = lo; t0 < hi; t0 += kThreads) {
+        const uint64_t t = t0 + threadIdx.x;
+        const unsigned long long w = t < hi ? static_cast<unsigned long long>(work(static_cast<uint32_t>(t))) : 0ull;
+        unsigned long long tot;
+        const unsigned long long ex = block_excl_scan64<kThreads>(w, tot);
+        if (t < hi) wpre[t] = run + ex;
+        run += tot;
+    }
+    if (threadIdx.x == 0) bsum[blockIdx.x] = run;
+}
+
+// Process all work of tasks [0, ntasks) (see file comment). `piece_head` must be 0 on
+// entry; bsum/wpre come from prep_items over a `nchunks`-block grid. smem: sboff holds
+// >= nchunks+1 entries. Returns the total work W.
+template <int kThreads, class Policy>
+__device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const unsigned long long* wpre,
+                              const unsigned long long* bsum, uint32_t nchunks, uint32_t* piece_head,
+                              unsigned long long* sboff) {
+    {
+        const uint32_t per = (nchunks + kThreads - 1) / kThreads;
+        const uint32_t c0 = threadIdx.x * per;
+        unsigned long long loc = 0;
+        for (uint32_t c = c0; c < c0 + per && c < nchunks; c++) loc += bsum[c];
+        unsigned long long tot;
+        unsigned long long run = block_excl_scan64<kThreads>(loc, tot);
+        for (uint32_t c = c0; c < c0 + per && c < nchunks; c++) {
+            sboff[c] = run;
+            run += bsum[c];
+        }
+        if (threadIdx.x == 0) sboff[nchunks] = tot;
+        __syncthreads();
+    }
+    const unsigned long long W = sboff[nchunks];
+    if (W == 0) return 0;
+    const uint32_t CH = chunk_len(ntasks, nchunks);
+    const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
+    unsigned long long PS = (W + 4ull * nwarps - 1) / (4ull * nwarps);
+    PS = (PS + 31) & ~31ull;
+    if (PS < 32) PS = 32;
+    const unsigned long long npieces = (W + PS - 1) / PS;
+    const uint32_t lane = lane_id();
+
+    while (true) {
+        uint32_t p = 0;
+        if (lane == 0) p = atomicAdd(piece_head, 1u);
+        p = __shfl_sync(kFull, p, 0);
+        if (p >= npieces) break;
+        const unsigned long long x0 = p * PS;
+        const unsigned long long x1 = x0 + PS < W ? x0 + PS : W;
+        // task containing x0: largest chunk c with sboff[c] <= x0, then largest t in it
+        uint32_t clo = 0, chi = nchunks;
+        while (chi - clo > 1) {
+            const uint32_t mid = (clo + chi) >> 1;
+            if (sboff[mid] <= x0) clo = mid; else chi = mid;
+        }
+        uint32_t ilo = clo * CH, ihi = min(ntasks, (clo + 1) * CH);
+        const unsigned long long rel = x0 - sboff[clo];
+        while (ihi - ilo > 1) {
+            const uint32_t mid = (ilo + ihi) >> 1;
+            if (wpre[mid] <= rel) ilo = mid; else ihi = mid;
+        }
+        uint32_t i = ilo;
+        // lanes hold tasks i..i+31 (start st); end_held = start of task i+32
+        uint32_t held = kNone;
+        ITask k{0, 0, 0, 0, 0, kNone};
+        unsigned long long st = ~0ull, end_held = ~0ull;
+        for (unsigned long long base = x0; base < x1;) {
+            if (held != i) {
+                const uint32_t t = i + lane;
+                if (t < ntasks) {
+                    k = P.load(t);
+                    st = sboff[t / CH] + wpre[t];
+                } else {
+                    st = ~0ull;
+                }
+                unsigned long long s32 = ~0ull;
+                if (lane == 31 && t + 1 < ntasks) s32 = sboff[(t + 1) / CH] + wpre[t + 1];
+                end_held = shfl64(s32, 31);
+                held = i;
+            }
+            const unsigned long long limit = x1 < end_held ? x1 : end_held;
+            const uint32_t relk = st <= base ? 0u
+                                  : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
+            const uint32_t own = warp_search_le(relk, lane);
+            const unsigned long long so = shfl64(st, own);
+            const ITask ko = shfl_task(k, own);
+            const unsigned long long x = base + lane;
+            uint32_t ja = 0, e = kNone;
+            const bool active = x < limit;
+            if (active) {
+                ja = static_cast<uint32_t>(x - so);
+                e = P.find(ko, P.elems[ko.oa + ja]);
+            }
+            P.visit(active, e != kNone, ko, ja, e);
+            const unsigned long long nb = base + 32 < limit ? base + 32 : limit;
+            i = (nb >= end_held) ? i + 32 : i + warp_search_le(relk, static_cast<uint32_t>(nb - base));
+            base = nb;
+        }
+    }
+    return W;
+}
+
+}  // namespace tdg

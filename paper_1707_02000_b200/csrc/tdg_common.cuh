@@ -127,8 +127,38 @@ __device__ __forceinline__ uint32_t queue_find(const uint2* q, uint32_t nq, uint
     return lo;
 }
 
+// ---- per-vertex neighbour -> edge-id hash tables (built once per graph, never compacted)
+// Table of x: htab[4*hoff4[x] .. 4*hoff4[x+1]), power-of-two size >= max(4, 2*d(x)),
+// linear probing. Entry = (value << 32) | key, key = neighbour id (kHEmpty = free slot),
+// value = edge id | (neighbour after x in the (degree, id) order ? 1<<31 : 0).
+constexpr uint32_t kHEmpty = 0xffffffffu;
+constexpr uint32_t kHUp = 0x80000000u;
+
+__device__ __forceinline__ uint32_t hmix(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x85ebca6bu;
+    x ^= x >> 13;
+    x *= 0xc2b2ae35u;
+    x ^= x >> 16;
+    return x;
+}
+
+// Value stored for `key` in the table at `tab` (mask = size-1), or kNone.
+__device__ __forceinline__ uint32_t hlookup(const unsigned long long* __restrict__ tab, uint32_t mask, uint32_t key) {
+    uint32_t h = hmix(key) & mask;
+    while (true) {
+        const unsigned long long e = tab[h];
+        const uint32_t k = static_cast<uint32_t>(e);
+        if (k == key) return static_cast<uint32_t>(e >> 32);
+        if (k == kHEmpty) return kNone;
+        h = (h + 1) & mask;
+    }
+}
+
 struct DevGraph {
     uint32_t n = 0, m = 0;
+    const uint32_t* hoff4 = nullptr;          // n+1, table offsets in units of 4 slots
+    const unsigned long long* htab = nullptr;  // hash table slots
     const uint32_t* off = nullptr;
     uint32_t* adj = nullptr;
     uint32_t* eid = nullptr;

@@ -34,6 +34,14 @@ size_t build_cub_bytes(uint32_t n, uint32_t m);
 cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_orientation,
                          cudaStream_t st, uint32_t* launches);
 
+// Per-vertex neighbour -> edge-id hash tables (tdg_common.cuh). hq: n+1 scratch; the host
+// reads hoff4[n] (total slots / 4) between the two calls to size htab.
+cudaError_t launch_htab_sizes(const uint32_t* off, uint32_t n, uint32_t* hq, uint32_t* hoff4, void* cub_tmp,
+                              size_t cub_bytes, cudaStream_t st, uint32_t* launches);
+cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, const uint32_t* eid,
+                             const uint32_t* hoff4, uint32_t m, unsigned long long* htab, uint64_t htab_slots,
+                             cudaStream_t st, uint32_t* launches);
+
 struct StatsAcc {
     unsigned long long d_max, sum_deg_sq, sum_dplus_sq, deg_sum_dplus_sq, deg_s1;
 };
@@ -42,15 +50,15 @@ cudaError_t launch_stats(const uint32_t* off, const uint32_t* eo, const uint32_t
 
 // ---- support (triangle.cpp:26-61 equivalent) ----
 struct SupportCtl {
-    unsigned long long big;  // packed (entries << 32 | pieces)
     unsigned long long tri3; // sum of supports
-    uint32_t piece_head, batch_head, overflow, smax;
+    uint32_t piece_head, overflow, smax, pad;
 };
-cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint2* queue, SupportCtl* ctl,
-                           int sm_count, cudaStream_t st, uint32_t* launches);
+constexpr uint32_t kMaxChunks = 2048;  // max blocks of a prep grid (one work chunk each)
+// wpre: >= m u64 scratch; bsum: kMaxChunks u64.
+cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* wpre, unsigned long long* bsum,
+                           SupportCtl* ctl, int sm_count, cudaStream_t st, uint32_t* launches);
 
 // ---- peel (truss_parallel.cpp:21-150 equivalent) ----
-constexpr uint32_t kMaxChunks = 2048;  // max blocks of the peel grid (one work chunk each)
 struct PhaseCtr {
     unsigned long long work; // sub-level: total probe items (informational)
     uint32_t out_size;       // list appends (curr for a scan, next for a sub-level)
@@ -72,10 +80,13 @@ struct PeelCtl {
     uint32_t pad;
     unsigned long long scan_ns;  // device-clock time in scan phases (leader thread)
     unsigned long long proc_ns;  // device-clock time in sub-level phases
+    unsigned long long probes;   // probe items over all sub-levels (sum of W)
+    unsigned long long hits;     // triangle visits (only when PeelBufs::count_hits)
+    unsigned long long dead;     // probes whose own slot was already processed (diagnostic)
 };
 struct PeelBufs {
-    uint32_t* s;
-    uint32_t* stamp;
+    uint32_t* s;               // support (u32): input of the peel / step-function I/O
+    unsigned long long* ss;    // packed per-edge state: (stamp << 32) | support
     uint32_t* L[2];
     uint32_t* A[2];
     unsigned long long* wpre;  // per curr position: exclusive work prefix inside its chunk
@@ -83,12 +94,13 @@ struct PeelBufs {
     PeelCtl* ctl;
     uint32_t* nsl;
     uint32_t nsl_cap;
+    uint32_t count_hits;  // diagnostic: count triangle visits (one atomic per warp step)
 };
 // Whole level loop in one persistent cooperative launch.
 cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cudaStream_t st,
                         uint32_t* launches);
 // truss[e] = s[e] + 2 and t_max.
-cudaError_t launch_finalize(const uint32_t* s, uint32_t m, uint32_t* truss, PeelCtl* ctl,
+cudaError_t launch_finalize(const unsigned long long* ss, uint32_t m, uint32_t* truss, PeelCtl* ctl,
                             cudaStream_t st, uint32_t* launches);
 
 // Step functions (tdg_scan / tdg_process_sublevel) on reference-style flags.
