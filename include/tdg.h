@@ -72,6 +72,7 @@ typedef struct tdg_times {
     double d2h_ms;      /* device -> host copy of the per-edge result                     */
     double total_ms;    /* whole call, device-side                                        */
     uint64_t triangles; /* sum(support) / 3                                               */
+    uint64_t support_probes; /* support-pass probe items (binary searches)                */
     uint64_t levels;    /* trace length = last non-empty level + 1                       */
     uint64_t sublevels; /* sum(nsl)                                                       */
     uint64_t scans;     /* scan passes actually executed (levels are skipped on device)   */

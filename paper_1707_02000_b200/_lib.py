@@ -46,7 +46,7 @@ class tdg_csr(C.Structure):
 class tdg_times(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("h2d_ms", "build_ms", "support_ms", "peel_ms", "scan_ms",
                                           "process_ms", "d2h_ms", "total_ms")] + \
-               [(k, C.c_uint64) for k in ("triangles", "levels", "sublevels", "scans", "compactions", "probes", "hits",
+               [(k, C.c_uint64) for k in ("triangles", "support_probes", "levels", "sublevels", "scans", "compactions", "probes", "hits",
                                           "dead_probes")] + \
                [("t_max", C.c_uint32), ("kernel_launches", C.c_uint32)]
 

@@ -131,6 +131,32 @@ __global__ void k_hinsert(const uint32_t* __restrict__ off, const uint32_t* __re
     }
 }
 
+// Support-pass task list: each oriented edge a->b is owned by the endpoint whose N+ list
+// is searched (the longer one; ties -> the source), and tasks are stored grouped by that
+// owner so consecutive tasks search the same L1-resident list. Slot j of owner x with
+// neighbour y is the task iff (x -> y and d+(x) >= d+(y)) or (y -> x and d+(y) < d+(x)).
+__global__ void k_svalid(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ src,
+                         const uint32_t* __restrict__ opos, uint32_t* __restrict__ flag, uint64_t slots) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t x = src[j], y = adj[j];
+        const uint32_t dx = opos[x + 1] - opos[x], dy = opos[y + 1] - opos[y];
+        flag[j] = flag[j] ? (dx >= dy ? 1u : 0u) : (dy < dx ? 1u : 0u);
+    }
+}
+
+__global__ void k_sscatter(const uint32_t* __restrict__ src, const uint32_t* __restrict__ flag,
+                           const uint32_t* __restrict__ pos, uint64_t slots, uint32_t* __restrict__ stask,
+                           uint32_t* __restrict__ sx) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        if (!flag[j]) continue;
+        const uint32_t t = pos[j];
+        stask[t] = static_cast<uint32_t>(j);
+        sx[t] = src[j];
+    }
+}
+
 struct MaxOp {
     __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
 };
@@ -210,6 +236,13 @@ cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_o
     if (err != cudaSuccess) return err;
     k_orient<<<gs, kThreads, 0, st>>>(b.adj, b.eid, b.el, b.flag, b.pos, slots, b.oadj, b.oeid, b.osrc);
     k_opos<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(b.off, b.pos, n, b.opos);
+    (*launches) += 2;
+    // support task list (flag/pos reused: orientation flags are consumed above)
+    k_svalid<<<gs, kThreads, 0, st>>>(b.adj, b.src, b.opos, b.flag, slots);
+    tmp = b.cub_bytes;
+    err = cub::DeviceScan::ExclusiveSum(b.cub_tmp, tmp, b.flag, b.pos, slots + 1, st);
+    if (err != cudaSuccess) return err;
+    k_sscatter<<<gs, kThreads, 0, st>>>(b.src, b.flag, b.pos, slots, b.stask, b.sx);
     (*launches) += 2;
     return cudaGetLastError();
 }

@@ -72,7 +72,7 @@ struct tdg_context {
     int sms = 148;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
-    DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc;
+    DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx;
     DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab;
     HostCtl* hctl = nullptr;
     cudaEvent_t ev[8] = {};
@@ -97,6 +97,8 @@ struct tdg_context {
         oadj.ensure(m * 4, "oadj");
         oeid.ensure(m * 4, "oeid");
         osrc.ensure(m * 4, "osrc");
+        stask.ensure(m * 4, "stask");
+        sx.ensure(m * 4, "sx");
         dl.ensure(n * 4, "dl");
         s.ensure(m * 4, "support");
         ctl.ensure(sizeof(PeelCtl), "ctl");
@@ -131,6 +133,8 @@ struct tdg_context {
         b.oadj = oadj.as<uint32_t>();
         b.oeid = oeid.as<uint32_t>();
         b.osrc = osrc.as<uint32_t>();
+        b.stask = stask.as<uint32_t>();
+        b.sx = sx.as<uint32_t>();
         b.cub_tmp = cub.p;
         b.cub_bytes = cub.cap;
         return b;
@@ -148,6 +152,8 @@ struct tdg_context {
         g.oadj = oadj.as<uint32_t>();
         g.oeid = oeid.as<uint32_t>();
         g.osrc = osrc.as<uint32_t>();
+        g.stask = stask.as<uint32_t>();
+        g.sx = sx.as<uint32_t>();
         g.hoff4 = hoff4.as<uint32_t>();
         g.htab = htab.as<unsigned long long>();
         return g;
@@ -171,7 +177,7 @@ struct tdg_context {
     }
     void trim() {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
-                         &osrc, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
+                         &osrc, &stask, &sx, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
                          &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab};
         for (DevBuf* b : all) b->release();
     }
@@ -304,6 +310,7 @@ void fill_times(tdg_times* t, tdg_context* c, bool host, bool peel) {
         t->total_ms = c->ms(0, 5);
     }
     t->triangles = c->hctl->sup.tri3 / 3;
+    t->support_probes = c->hctl->sup.probes;
     t->kernel_launches = c->launches;
 }
 

@@ -168,6 +168,8 @@ struct DevGraph {
     const uint32_t* oadj = nullptr;
     const uint32_t* oeid = nullptr;
     const uint32_t* osrc = nullptr;
+    const uint32_t* stask = nullptr;  // support tasks (slot index), see build.cu k_svalid
+    const uint32_t* sx = nullptr;     // owner vertex of each support task's slot
 };
 
 }  // namespace tdg

@@ -26,6 +26,8 @@ struct BuildBufs {
     uint32_t* oadj;        // m
     uint32_t* oeid;        // m
     uint32_t* osrc;        // m
+    uint32_t* stask;       // m  support tasks: slot index, grouped by searched-list owner
+    uint32_t* sx;          // m  owner of that slot
     void* cub_tmp;
     size_t cub_bytes;
 };
@@ -52,6 +54,7 @@ cudaError_t launch_stats(const uint32_t* off, const uint32_t* eo, const uint32_t
 struct SupportCtl {
     unsigned long long tri3; // sum of supports
     uint32_t piece_head, overflow, smax, pad;
+    unsigned long long probes;  // probe items of the support pass
 };
 constexpr uint32_t kMaxChunks = 2048;  // max blocks of a prep grid (one work chunk each)
 // wpre: >= m u64 scratch; bsum: kMaxChunks u64.
