@@ -325,7 +325,7 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         stage_and_build(c, g, d, host, true, true);
         c->ensure_peel(d.n, d.m);
         const DevGraph dg = c->dev_graph(d.n, d.m);
-        ck(launch_support(dg, c->s.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
+        ck(launch_support(dg, c->s.as<uint32_t>(), c->flag.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
                           c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
         uint32_t* sup_dev = nullptr;
         if (support_out && d.m) {
@@ -384,7 +384,7 @@ int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_
         stage_and_build(c, g, d, host, true, true);
         const DevGraph dg = c->dev_graph(d.n, d.m);
         uint32_t* sdev = host ? c->s.as<uint32_t>() : support_out;
-        ck(launch_support(dg, sdev, c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
+        ck(launch_support(dg, sdev, c->flag.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
                           c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
         ck(cudaEventRecord(c->ev[3], c->stream), "event");
         if (host && d.m)

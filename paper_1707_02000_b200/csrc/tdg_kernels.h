@@ -57,9 +57,10 @@ struct SupportCtl {
     unsigned long long probes;  // probe items of the support pass
 };
 constexpr uint32_t kMaxChunks = 2048;  // max blocks of a prep grid (one work chunk each)
-// wpre: >= m u64 scratch; bsum: kMaxChunks u64.
-cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* wpre, unsigned long long* bsum,
-                           SupportCtl* ctl, int sm_count, cudaStream_t st, uint32_t* launches);
+// ocnt: m u32 scratch (per oriented slot); wpre: >= m u64 scratch; bsum: kMaxChunks u64.
+cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint32_t* ocnt, unsigned long long* wpre,
+                           unsigned long long* bsum, SupportCtl* ctl, int sm_count, cudaStream_t st,
+                           uint32_t* launches);
 
 // ---- peel (truss_parallel.cpp:21-150 equivalent) ----
 struct PhaseCtr {
