@@ -10,6 +10,8 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "tdg.h"
 #include "tdg_kernels.h"
@@ -73,7 +75,7 @@ struct tdg_context {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx;
-    DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab;
+    DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab, Ls, bhist, bcur, trace;
     HostCtl* hctl = nullptr;
     cudaEvent_t ev[8] = {};
     uint32_t launches = 0;
@@ -113,6 +115,12 @@ struct tdg_context {
         L1.ensure(m * 4, "L1");
         A0.ensure(m * 4, "A0");
         A1.ensure(m * 4, "A1");
+        Ls.ensure(m * 4, "Ls");
+        if (bhist.cap == 0) {
+            bhist.ensure(kBuckets * 4, "bhist");
+            ck(cudaMemset(bhist.p, 0, kBuckets * 4), "memset");
+        }
+        bcur.ensure(kBuckets * 4, "bcur");
         nsl.ensure((n + 2) * 4, "nsl");
     }
 
@@ -173,12 +181,24 @@ struct tdg_context {
         p.nsl_cap = n + 1;
         const char* ch = std::getenv("TDG_COUNT_HITS");
         p.count_hits = (ch && ch[0] == '1') ? 1u : 0u;
+        p.Ls = Ls.as<uint32_t>();
+        p.bhist = bhist.as<uint32_t>();
+        p.bcur = bcur.as<uint32_t>();
+        uint32_t bits = 0;
+        while ((1ull << bits) < n) bits++;
+        p.bshift = bits > 16 ? bits - 16 : 0;
+        p.trace = nullptr;
+        p.trace_cap = 0;
+        if (std::getenv("TDG_TRACE")) {
+            p.trace = trace.as<unsigned long long>();
+            p.trace_cap = static_cast<uint32_t>(trace.cap / 32);
+        }
         return p;
     }
     void trim() {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
                          &osrc, &stask, &sx, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
-                         &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab};
+                         &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &Ls, &bhist, &bcur, &trace};
         for (DevBuf* b : all) b->release();
     }
     float ms(int a, int b) const {
@@ -324,6 +344,7 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         c->launches = 0;
         stage_and_build(c, g, d, host, true, true);
         c->ensure_peel(d.n, d.m);
+        if (std::getenv("TDG_TRACE")) c->trace.ensure(size_t(32) << 20, "trace");
         const DevGraph dg = c->dev_graph(d.n, d.m);
         ck(launch_support(dg, c->s.as<uint32_t>(), c->flag.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
                           c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
@@ -353,6 +374,17 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         if (pc.overflow || c->hctl->sup.overflow)
             throw Fail{TDG_ERR_RANGE, "work queue exceeded 32-bit piece counter"};
         const uint64_t len = d.m ? pc.levels_len : 0;
+        if (const char* tp = std::getenv("TDG_TRACE")) {  // diagnostic dump: level, cs, W, ns, K
+            const size_t k = std::min<size_t>(pc.sublevels, c->trace.cap / 32);
+            std::vector<unsigned long long> h(4 * k);
+            if (k) ck(cudaMemcpy(h.data(), c->trace.p, 32 * k, cudaMemcpyDeviceToHost), "D2H trace");
+            if (FILE* f = std::fopen(tp, "w")) {
+                for (size_t i = 0; i < k; i++)
+                    std::fprintf(f, "%llu %llu %llu %llu %llu\n", h[4 * i] >> 32, h[4 * i] & 0xffffffffull, h[4 * i + 1],
+                                 h[4 * i + 2], h[4 * i + 3]);
+                std::fclose(f);
+            }
+        }
         if (nsl_len) *nsl_len = len;
         if (nsl_out && len) {
             const uint64_t k = len < nsl_cap ? len : nsl_cap;

@@ -157,12 +157,29 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
         unsigned long long st = ~0ull, end_held = ~0ull;
         for (unsigned long long base = x0; base < x1;) {
             if (held != i) {
+                // Slide the held window: tasks already held move down by `adv` lanes with
+                // shuffles; only the lanes past the old window load (each task descriptor
+                // costs ~6 random loads, so reloading all 32 per step dominated traffic).
+                const uint32_t adv = (held != kNone && i > held) ? i - held : 32u;
+                if (adv < 32) {
+                    k.id = __shfl_down_sync(kFull, k.id, adv);
+                    k.oa = __shfl_down_sync(kFull, k.oa, adv);
+                    k.la = __shfl_down_sync(kFull, k.la, adv);
+                    k.ob = __shfl_down_sync(kFull, k.ob, adv);
+                    k.lb = __shfl_down_sync(kFull, k.lb, adv);
+                    k.aux = __shfl_down_sync(kFull, k.aux, adv);
+                    const uint32_t lo = __shfl_down_sync(kFull, static_cast<uint32_t>(st), adv);
+                    const uint32_t hi = __shfl_down_sync(kFull, static_cast<uint32_t>(st >> 32), adv);
+                    st = (static_cast<unsigned long long>(hi) << 32) | lo;
+                }
                 const uint32_t t = i + lane;
-                if (t < ntasks) {
-                    k = P.load(t);
-                    st = sboff[t / CH] + wpre[t];
-                } else {
-                    st = ~0ull;
+                if (lane + adv >= 32) {
+                    if (t < ntasks) {
+                        k = P.load(t);
+                        st = sboff[t / CH] + wpre[t];
+                    } else {
+                        st = ~0ull;
+                    }
                 }
                 unsigned long long s32 = ~0ull;
                 if (lane == 31 && t + 1 < ntasks) s32 = sboff[(t + 1) / CH] + wpre[t + 1];

@@ -230,6 +230,74 @@ __device__ void phase_scan(unsigned long long* ss, uint32_t level, uint32_t K, c
 }
 
 // Sub-level prep: block b owns curr chunk b; probe count of e1 = min live degree.
+// ---- locality: order a big sub-level's curr edges by the vertex whose hash table they
+// probe (bucketed counting sort, 2^16 buckets of 2^bshift vertices), so concurrently
+// running warps share hot tables in L2 instead of hitting DRAM for every lookup.
+#ifndef TDG_SORT_MIN
+#define TDG_SORT_MIN (1u << 20)
+#endif
+constexpr uint32_t kSortMin = TDG_SORT_MIN;
+
+__device__ __forceinline__ uint32_t searched_vertex(const DevGraph& g, uint32_t e1) {
+    const uint2 p = g.el[e1];
+    return g.dl[p.x] <= g.dl[p.y] ? p.y : p.x;  // same choice as ptask
+}
+
+// Warp-aggregated bucket counter increment; returns this lane's rank among the lanes of
+// its warp with the same bucket plus the counter's old value (all lanes must call).
+__device__ __forceinline__ uint32_t bucket_add(uint32_t* ctr, uint32_t bucket, bool valid) {
+    const uint32_t vm = __ballot_sync(kFull, valid);
+    uint32_t pos = 0;
+    if (valid) {
+        const uint32_t grp = __match_any_sync(vm, bucket);
+        const uint32_t leader = __ffs(grp) - 1;
+        uint32_t base = 0;
+        if (lane_id() == leader) base = atomicAdd(&ctr[bucket], static_cast<uint32_t>(__popc(grp)));
+        base = __shfl_sync(grp, base, leader);
+        pos = base + __popc(grp & lanemask_lt());
+    }
+    return pos;
+}
+
+__device__ void phase_bucket_hist(const DevGraph& g, const uint32_t* curr, uint32_t cs, uint32_t* hist, uint32_t shift) {
+    for (uint64_t i0 = uint64_t(blockIdx.x) * kPeelThreads + (threadIdx.x & ~31u); i0 < cs;
+         i0 += uint64_t(gridDim.x) * kPeelThreads) {
+        const uint64_t i = i0 + lane_id();
+        const bool valid = i < cs;
+        const uint32_t bk = valid ? (searched_vertex(g, curr[i]) >> shift) : 0;
+        bucket_add(hist, bk, valid);
+    }
+}
+
+// One block: cursor = exclusive scan of hist; hist is cleared for the next use.
+__device__ void phase_bucket_scan(uint32_t* hist, uint32_t* cursor) {
+    constexpr uint32_t per = kBuckets / kPeelThreads;
+    const uint32_t c0 = threadIdx.x * per;
+    unsigned long long loc = 0;
+    for (uint32_t c = 0; c < per; c++) loc += hist[c0 + c];
+    unsigned long long tot;
+    unsigned long long run = block_excl_scan64<kPeelThreads>(loc, tot);
+    for (uint32_t c = 0; c < per; c++) {
+        const uint32_t h = hist[c0 + c];
+        cursor[c0 + c] = static_cast<uint32_t>(run);
+        hist[c0 + c] = 0;
+        run += h;
+    }
+}
+
+__device__ void phase_bucket_scatter(const DevGraph& g, const uint32_t* curr, uint32_t cs, uint32_t* cursor,
+                                     uint32_t shift, uint32_t* out) {
+    for (uint64_t i0 = uint64_t(blockIdx.x) * kPeelThreads + (threadIdx.x & ~31u); i0 < cs;
+         i0 += uint64_t(gridDim.x) * kPeelThreads) {
+        const uint64_t i = i0 + lane_id();
+        const bool valid = i < cs;
+        const uint32_t e = valid ? curr[i] : 0;
+        const uint32_t bk = valid ? (searched_vertex(g, e) >> shift) : 0;
+        const uint32_t pos = bucket_add(cursor, bk, valid);
+        if (valid) out[pos] = e;
+    }
+}
+
 __device__ void phase_prep(const DevGraph& g, const uint32_t* curr, uint32_t cs, unsigned long long* wpre,
                            unsigned long long* bsum) {
     prep_items<kPeelThreads>(cs, [&](uint32_t t) {
@@ -356,6 +424,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
     uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m;
     bool implicit = true;
     unsigned long long t_prev = leader ? gtimer() : 0;
+    unsigned long long sub_w = 0;
     while (true) {
         // ---- scan at `level` (one grid barrier)
         if (leader) { reset_ctr(&ctl->ph[(j + 1) % 3]); ctl->scans++; }
@@ -394,15 +463,40 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                 reset_ctr(&ctl->ph[(j + 1) % 3]);
             }
             if (level > 0) {  // level 0: s[e1] == 0 bounds its live triangles to none
-                phase_prep(g, pb.L[li], cs, pb.wpre, pb.bsum);
+                const uint32_t* tasks = pb.L[li];
+                if (kSortMin && cs >= kSortMin) {  // group big sub-levels by searched vertex
+                    phase_bucket_hist(g, tasks, cs, pb.bhist, pb.bshift);
+                    grid.sync();
+                    if (blockIdx.x == 0) phase_bucket_scan(pb.bhist, pb.bcur);
+                    grid.sync();
+                    phase_bucket_scatter(g, tasks, cs, pb.bcur, pb.bshift, pb.Ls);
+                    grid.sync();
+                    tasks = pb.Ls;
+                }
+                phase_prep(g, tasks, cs, pb.wpre, pb.bsum);
                 grid.sync();
                 const unsigned long long W =
-                    phase_process(g, pb.ss, level, K, pb.L[li], cs, pb.wpre, pb.bsum, gridDim.x,
+                    phase_process(g, pb.ss, level, K, tasks, cs, pb.wpre, pb.bsum, gridDim.x,
                                   &ctl->ph[j % 3], pb.L[li ^ 1], pb.count_hits ? &ctl->hits : nullptr);
-                if (leader) ctl->probes += W;
+                if (leader) {
+                    ctl->probes += W;
+                    sub_w = W;
+                }
             }
             grid.sync();
-            if (leader) { const unsigned long long t = gtimer(); ctl->proc_ns += t - t_prev; t_prev = t; }
+            if (leader) {
+                const unsigned long long t = gtimer();
+                if (pb.trace && ctl->sublevels <= pb.trace_cap) {  // diagnostic per-sub-level record
+                    unsigned long long* r4 = pb.trace + 4ull * (ctl->sublevels - 1);
+                    r4[0] = (static_cast<unsigned long long>(level) << 32) | cs;
+                    r4[1] = sub_w;
+                    r4[2] = t - t_prev;
+                    r4[3] = K;
+                }
+                ctl->proc_ns += t - t_prev;
+                t_prev = t;
+                sub_w = 0;
+            }
             j++;
             K++;
             r = &ctl->ph[(j - 1) % 3];

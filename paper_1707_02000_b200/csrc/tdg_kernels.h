@@ -99,7 +99,14 @@ struct PeelBufs {
     uint32_t* nsl;
     uint32_t nsl_cap;
     uint32_t count_hits;  // diagnostic: count triangle visits (one atomic per warp step)
+    uint32_t* Ls;         // m: a big sub-level's curr list reordered by searched vertex
+    uint32_t* bhist;      // kBuckets counters (zero between uses)
+    uint32_t* bcur;       // kBuckets cursors
+    uint32_t bshift;      // bucket = vertex >> bshift
+    unsigned long long* trace;  // diagnostic (TDG_TRACE): 4 words per sub-level, or null
+    uint32_t trace_cap;
 };
+constexpr uint32_t kBuckets = 1u << 16;
 // Whole level loop in one persistent cooperative launch.
 cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cudaStream_t st,
                         uint32_t* launches);
