@@ -186,7 +186,26 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
                 end_held = shfl64(s32, 31);
                 held = i;
             }
-            const unsigned long long limit = x1 < end_held ? x1 : end_held;
+            unsigned long long limit = x1 < end_held ? x1 : end_held;
+            if (Policy::kHasStaged) {
+                // STAGED tasks (long, comparable lists) run alone over their in-piece range;
+                // the window below stops at the first staged task it holds.
+                const uint32_t smask = __ballot_sync(kFull, P.staged(k));
+                if (smask & 1u) {
+                    const unsigned long long st0 = shfl64(st, 0), st1 = shfl64(st, 1);
+                    const unsigned long long end0 = st1 < end_held ? st1 : end_held;
+                    const unsigned long long lim0 = x1 < end0 ? x1 : end0;
+                    P.staged_range(shfl_task(k, 0), static_cast<uint32_t>(base - st0),
+                                   static_cast<uint32_t>(lim0 - st0));
+                    if (lim0 == end0) i += 1;
+                    base = lim0;
+                    continue;
+                }
+                if (smask) {
+                    const unsigned long long sm = shfl64(st, __ffs(smask) - 1);
+                    limit = sm < limit ? sm : limit;
+                }
+            }
             const uint32_t relk = st <= base ? 0u
                                   : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
             const uint32_t own = warp_search_le(relk, lane);

@@ -54,20 +54,39 @@ constexpr int kPeelThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kWarps = kPeelThreads / 32;
 
-// Task of e1 = (u,v): probe the shorter live list against the other endpoint's hash table
-// (id = e1, aux = the searched endpoint, which never occurs in its own table).
+// Task of e1 = (u,v): probe the shorter live list a against the other endpoint b (id = e1,
+// aux = b, which never occurs in its own lists). Two forms:
+//  * HASH   (default): ob/lb = b's hash table (quad offset, slot mask);
+//  * STAGED (both lists long and of comparable length): ob = off[b], lb = dl[b] | kStaged;
+//    the piece's slice of N(b) is staged in shared memory and searched there (PeelPolicy).
+constexpr uint32_t kStaged = 0x80000000u;
+#ifndef TDG_STAGE_MIN
+#define TDG_STAGE_MIN 128  // probe-list length from which a task may be staged
+#endif
+#ifndef TDG_STAGE_RATIO
+#define TDG_STAGE_RATIO 8  // ... if the searched list is at most this many times longer
+#endif
+constexpr uint32_t kStageA = 128;  // probe elements per staged chunk
+constexpr uint32_t kStageB = 768;  // max searched-list slice held in shared memory (per warp)
+
 __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
     const uint2 p = g.el[e1];
     const uint32_t du = g.dl[p.x], dv = g.dl[p.y];
     const bool pu = du <= dv;
     const uint32_t a = pu ? p.x : p.y, b = pu ? p.y : p.x;
+    const uint32_t la = pu ? du : dv, lbl = pu ? dv : du;
     ITask k;
     k.id = e1;
     k.oa = g.off[a];
-    k.la = pu ? du : dv;
-    k.ob = g.hoff4[b];
-    k.lb = 4u * (g.hoff4[b + 1] - k.ob) - 1u;
+    k.la = la;
     k.aux = b;
+    if (TDG_STAGE_MIN && la >= TDG_STAGE_MIN && static_cast<uint64_t>(lbl) <= static_cast<uint64_t>(la) * TDG_STAGE_RATIO) {
+        k.ob = g.off[b];
+        k.lb = lbl | kStaged;
+    } else {
+        k.ob = g.hoff4[b];
+        k.lb = 4u * (g.hoff4[b + 1] - k.ob) - 1u;
+    }
     return k;
 }
 
@@ -132,7 +151,63 @@ struct PeelPolicy {
     uint32_t* next;
     const uint32_t* elems;
     unsigned long long* hit_ctr;  // diagnostic, may be null
+    uint32_t* stage;              // this warp's kStageB-entry shared buffer
+    static constexpr bool kHasStaged = true;
     __device__ ITask load(uint32_t t) const { return ptask(g, curr[t]); }
+    __device__ bool staged(const ITask& k) const { return (k.lb & kStaged) != 0; }
+    // A STAGED task's probe range [j0, j1): per kStageA-element chunk of N(a), the matching
+    // slice of N(b) (it starts where the previous one ended: both lists are sorted) is copied
+    // to shared memory with coalesced loads and searched there; a slice longer than kStageB
+    // (a locally skewed chunk) falls back to hash lookups.
+    __device__ void staged_range(const ITask& k, uint32_t j0, uint32_t j1) const {
+        const uint32_t lane = lane_id();
+        const uint32_t* A = g.adj + k.oa;
+        const uint32_t* B = g.adj + k.ob;
+        const uint32_t nbt = k.lb & ~kStaged, b = k.aux;
+        uint32_t lo = 0;
+        if (lane == 0) lo = lower_bound_u32(B, nbt, A[j0]);
+        lo = __shfl_sync(kFull, lo, 0);
+        for (uint32_t c0 = j0; c0 < j1; c0 += kStageA) {
+            const uint32_t c1 = min(j1, c0 + kStageA);
+            uint32_t hi = 0;
+            if (lane == 0) hi = lo + upper_bound_u32(B + lo, nbt - lo, A[c1 - 1]);
+            hi = __shfl_sync(kFull, hi, 0);
+            const uint32_t nbr = hi - lo;
+            if (nbr <= kStageB) {
+                for (uint32_t q = lane; q < nbr; q += 32) stage[q] = B[lo + q];
+                __syncwarp();
+                for (uint32_t r = c0; r < c1; r += 32) {
+                    const uint32_t ja = r + lane;
+                    const bool active = ja < c1;
+                    uint32_t eb = kNone;
+                    if (active) {
+                        const uint32_t x = A[ja];
+                        const uint32_t pp = lower_bound_u32(stage, nbr, x);
+                        if (pp < nbr && stage[pp] == x) eb = g.eid[k.ob + lo + pp];
+                    }
+                    visit(active, eb != kNone, k, ja, eb);
+                }
+                __syncwarp();
+            } else {
+                const uint32_t q4 = g.hoff4[b];
+                const uint32_t mask = 4u * (g.hoff4[b + 1] - q4) - 1u;
+                for (uint32_t r = c0; r < c1; r += 32) {
+                    const uint32_t ja = r + lane;
+                    const bool active = ja < c1;
+                    uint32_t eb = kNone;
+                    if (active) {
+                        const uint32_t x = A[ja];
+                        if (x != b) {
+                            const uint32_t v = hlookup(g.htab + 4ull * q4, mask, x);
+                            eb = v == kNone ? kNone : (v & ~kHUp);
+                        }
+                    }
+                    visit(active, eb != kNone, k, ja, eb);
+                }
+            }
+            lo = hi;
+        }
+    }
     __device__ uint32_t find(const ITask& k, uint32_t x) const {
         if (x == k.aux) return kNone;
         const uint32_t v = hlookup(g.htab + 4ull * k.ob, k.lb, x);
@@ -313,7 +388,8 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             uint32_t nchunks, PhaseCtr* ph, uint32_t* next,
                                             unsigned long long* hit_ctr) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
-    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr};
+    __shared__ uint32_t sstage[kWarps * kStageB];
+    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }
 

@@ -47,7 +47,10 @@ struct SupportPolicy {
     uint32_t* s;
     uint32_t* ocnt;
     const uint32_t* elems;
+    static constexpr bool kHasStaged = false;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
+    __device__ bool staged(const ITask&) const { return false; }
+    __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
     __device__ uint32_t find(const ITask& k, uint32_t x) const {
         const uint32_t p = lower_bound_u32(g.oadj + k.ob, k.lb, x);
         return (p < k.lb && g.oadj[k.ob + p] == x) ? p : kNone;

@@ -56,7 +56,7 @@ struct SupportCtl {
     uint32_t piece_head, overflow, smax, pad;
     unsigned long long probes;  // probe items of the support pass
 };
-constexpr uint32_t kMaxChunks = 2048;  // max blocks of a prep grid (one work chunk each)
+constexpr uint32_t kMaxChunks = 1024;  // max blocks of a prep grid (one work chunk each)
 // ocnt: m u32 scratch (per oriented slot); wpre: >= m u64 scratch; bsum: kMaxChunks u64.
 cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint32_t* ocnt, unsigned long long* wpre,
                            unsigned long long* bsum, SupportCtl* ctl, int sm_count, cudaStream_t st,
