@@ -294,6 +294,11 @@ def bench_ours(args):
                 else "k_support", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes": k_bytes,
                 "kernel_ms": k_ms,
+                # The SURVEY §8(d) model charges PKT's full-list scans (4*S2); hash / staged
+                # lookups touch far less, so the model fraction can exceed 1. The hardware
+                # figure: ncu DRAM bytes of this kernel (profiles/ncu_traffic.json) over its time.
+                "dram_frac_ncu": (traffic / (k_ms * 1e-3) / 1e9 / peak) if traffic else None,
+                "model": "B_peel = 4*S2 + 48*T + 55*m + 5*sum(tau-1); B_sup = 4*S1 + 24*m + 32*T (SURVEY 8d)",
                 "other": {"support": {"bytes": b_sup, "ms": avg["support_ms"],
                                       "GBps": b_sup / (avg["support_ms"] * 1e-3) / 1e9},
                           "peel": {"bytes": b_peel, "ms": avg["peel_ms"],
