@@ -13,6 +13,7 @@
  *   tdg_build_truss_graph<- trussdec::build_truss_graph(const CsrGraph&)
  *                           proj/include/trussdec/graph.hpp:69, proj/src/graph.cpp:73-101
  *   tdg_stats            <- trussdec::stats(const CsrGraph&)  proj/src/graph.cpp:135-150
+ *   tdg_triangle_count   <- trussdec::triangle_count(const TrussGraph&, int)  triangle.cpp:90-116
  *   tdg_scan             <- trussdec::scan(...)              truss_parallel.hpp:62, .cpp:21-37
  *   tdg_process_sublevel <- trussdec::process_sublevel(...)  truss_parallel.hpp:67-68, .cpp:39-104
  *
@@ -124,6 +125,10 @@ int tdg_support_device(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out
 /* build_truss_graph: eo[n], eid[2m], el[2m] (el[2e], el[2e+1] = u < v). Host pointers. */
 int tdg_build_truss_graph(tdg_context* ctx, const tdg_csr* g, uint32_t* eo, uint32_t* eid,
                           uint32_t* el);
+
+/* triangle_count (proj/src/triangle.cpp:90-116): number of triangles.
+ * Host-pointer graph. */
+int tdg_triangle_count(tdg_context* ctx, const tdg_csr* g, uint64_t* count, tdg_times* times);
 
 /* stats (host-pointer graph). */
 int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out);

@@ -517,6 +517,27 @@ int tdg_build_truss_graph(tdg_context* ctx, const tdg_csr* g, uint32_t* eo, uint
     });
 }
 
+int tdg_triangle_count(tdg_context* ctx, const tdg_csr* g, uint64_t* count, tdg_times* times) {
+    return guarded([&] {
+        if (!count) throw Fail{TDG_ERR_INVALID, "count is NULL"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, true);
+        c->launches = 0;
+        stage_and_build(c, g, d, true, true, false);
+        ck(launch_triangle_count(c->dev_graph(d.n, d.m), c->src.as<unsigned long long>(),
+                                 c->bsum.as<unsigned long long>(), c->sctl.as<SupportCtl>(), c->sms, c->stream,
+                                 &c->launches), "triangle count");
+        ck(cudaEventRecord(c->ev[3], c->stream), "event");
+        ck(cudaEventRecord(c->ev[5], c->stream), "event");
+        ck(cudaMemcpyAsync(&c->hctl->sup, c->sctl.p, sizeof(SupportCtl), cudaMemcpyDeviceToHost, c->stream), "D2H sctl");
+        ck(cudaStreamSynchronize(c->stream), "triangle count");
+        *count = c->hctl->sup.tri3;
+        fill_times(times, c, true, false);
+        if (times) times->triangles = *count;
+    });
+}
+
 int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out) {
     return guarded([&] {
         if (!out) throw Fail{TDG_ERR_INVALID, "out is NULL"};

@@ -77,6 +77,35 @@ __global__ void __launch_bounds__(kThreads) k_support_prep(DevGraph g, unsigned 
     }, wpre, bsum);
 }
 
+// triangle_count (triangle.cpp:90-116): the same task stream with no per-edge writes; each
+// warp keeps a register count of its hits and adds it once at the end.
+struct CountPolicy {
+    const DevGraph& g;
+    const uint32_t* elems;
+    unsigned long long count = 0;
+    static constexpr bool kHasStaged = false;
+    __device__ ITask load(uint32_t t) const { return otask(g, t); }
+    __device__ bool staged(const ITask&) const { return false; }
+    __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
+    __device__ uint32_t find(const ITask& k, uint32_t x) const {
+        const uint32_t p = lower_bound_u32(g.oadj + k.ob, k.lb, x);
+        return (p < k.lb && g.oadj[k.ob + p] == x) ? p : kNone;
+    }
+    __device__ void visit(bool, bool hit, const ITask&, uint32_t, uint32_t) {
+        count += static_cast<unsigned long long>(__popc(__ballot_sync(kFull, hit)));
+    }
+};
+
+__global__ void __launch_bounds__(kThreads) k_triangle_count(DevGraph g, const unsigned long long* wpre,
+                                                             const unsigned long long* bsum, uint32_t nchunks,
+                                                             SupportCtl* ctl) {
+    __shared__ unsigned long long sboff[kMaxChunks + 1];
+    CountPolicy P{g, g.oadj};
+    const unsigned long long W = process_items<kThreads>(P, g.m, wpre, bsum, nchunks, &ctl->piece_head, sboff);
+    if (lane_id() == 0 && P.count) atomicAdd(&ctl->tri3, P.count);
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->probes = W;
+}
+
 __global__ void __launch_bounds__(kThreads) k_support(DevGraph g, uint32_t* __restrict__ s, uint32_t* __restrict__ ocnt,
                                                       const unsigned long long* wpre, const unsigned long long* bsum,
                                                       uint32_t nchunks, SupportCtl* ctl) {
@@ -133,6 +162,21 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint32_t* ocnt, unsig
     k_support_combine<<<grid, kThreads, 0, st>>>(g.oeid, ocnt, g.m, s);
     k_support_sum<<<grid, kThreads, 0, st>>>(s, g.m, ctl);
     (*launches) += 4;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_triangle_count(const DevGraph& g, unsigned long long* wpre, unsigned long long* bsum,
+                                  SupportCtl* ctl, int sm_count, cudaStream_t st, uint32_t* launches) {
+    cudaError_t err = cudaMemsetAsync(ctl, 0, sizeof(SupportCtl), st);
+    if (err != cudaSuccess || g.m == 0) return err;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_triangle_count, kThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    const unsigned grid = static_cast<unsigned>(sm_count * per_sm);
+    const unsigned nchunks = grid < kMaxChunks ? grid : kMaxChunks;
+    k_support_prep<<<nchunks, kThreads, 0, st>>>(g, wpre, bsum);
+    k_triangle_count<<<grid, kThreads, 0, st>>>(g, wpre, bsum, nchunks, ctl);
+    (*launches) += 2;
     return cudaGetLastError();
 }
 

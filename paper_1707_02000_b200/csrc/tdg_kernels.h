@@ -62,6 +62,10 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint32_t* ocnt, unsig
                            unsigned long long* bsum, SupportCtl* ctl, int sm_count, cudaStream_t st,
                            uint32_t* launches);
 
+// triangle_count (triangle.cpp:90-116): count lands in ctl->tri3 (= T, not 3T).
+cudaError_t launch_triangle_count(const DevGraph& g, unsigned long long* wpre, unsigned long long* bsum,
+                                  SupportCtl* ctl, int sm_count, cudaStream_t st, uint32_t* launches);
+
 // ---- peel (truss_parallel.cpp:21-150 equivalent) ----
 struct PhaseCtr {
     unsigned long long work; // sub-level: total probe items (informational)

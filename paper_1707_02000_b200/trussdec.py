@@ -6,6 +6,7 @@ Names, argument meaning and error behaviour follow the reference (paths relative
   build_truss_graph(CsrGraph) -> TrussGraph              include/trussdec/graph.hpp:69
   stats(CsrGraph) -> GraphStats                          graph.hpp:74
   support_am4(TrussGraph, workers) -> SupportArray       include/trussdec/triangle.hpp:16
+  triangle_count(TrussGraph, workers) -> int             triangle.hpp:19 (triangle.cpp:90-116)
   truss_parallel(TrussGraph, workers) -> ParallelDecomposition
                                                          include/trussdec/truss_parallel.hpp:72
   scan(s, level, LevelFrontier, workers)                 truss_parallel.hpp:62
@@ -255,6 +256,12 @@ class Context:
         _ck(_lib.tdg().tdg_build_truss_graph(self._h, C.byref(v), eo.ctypes.data, eid.ctypes.data, el.ctypes.data))
         return TrussGraph(g, eid[: 2 * g.m], el[: 2 * g.m].reshape(-1, 2), eo[: g.n])
 
+    def triangle_count(self, g: CsrGraph) -> int:
+        cnt = C.c_uint64()
+        v = g._view()
+        _ck(_lib.tdg().tdg_triangle_count(self._h, C.byref(v), C.byref(cnt), None))
+        return cnt.value
+
     def stats(self, g: CsrGraph) -> GraphStats:
         st = tdg_graph_stats()
         v = g._view()
@@ -281,6 +288,12 @@ def build_truss_graph(g: CsrGraph) -> TrussGraph:
 
 def stats(g: CsrGraph) -> GraphStats:
     return default_context().stats(g)
+
+
+def triangle_count(tg: TrussGraph | CsrGraph, workers: int = 1) -> int:
+    """triangle.cpp:90-116."""
+    g = tg.csr if isinstance(tg, TrussGraph) else tg
+    return default_context().triangle_count(g)
 
 
 def support_am4(tg: TrussGraph | CsrGraph, workers: int = 1) -> np.ndarray:

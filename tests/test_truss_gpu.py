@@ -242,3 +242,16 @@ def test_bad_input_raises(td):
     g = td.CsrGraph(3, 2, np.array([0, 1, 2, 3], np.int64), np.array([1, 0, 2, 1], np.int32))
     with pytest.raises(ValueError):
         td.truss_parallel(g)  # offsets[n] != 2m
+
+
+@pytest.mark.parametrize("rec", FIXTURES[::3], ids=lambda r: r["name"])
+def test_triangle_count_matches_reference(td, oracle, rec):
+    """triangle.cpp:90-116 against the reference's own count."""
+    assert td.triangle_count(gpu_graph(build_fixture(oracle, rec))) == rec["triangles"]
+
+
+def test_triangle_count_closed_forms(td, oracle):
+    """test_triangle.cpp:42-52: K5 has C(5,3) = 10 triangles, K3,3 none."""
+    assert td.triangle_count(gpu_graph(oracle.complete_graph(5))) == 10
+    k33 = oracle.canonicalize([(a, b) for a in range(3) for b in range(3, 6)])
+    assert td.triangle_count(gpu_graph(k33)) == 0
