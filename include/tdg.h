@@ -14,6 +14,7 @@
  *                           proj/include/trussdec/graph.hpp:69, proj/src/graph.cpp:73-101
  *   tdg_stats            <- trussdec::stats(const CsrGraph&)  proj/src/graph.cpp:135-150
  *   tdg_triangle_count   <- trussdec::triangle_count(const TrussGraph&, int)  triangle.cpp:90-116
+ *   tdg_ktruss_components<- trussdec::ktruss_subgraphs(tg, res, k)  truss_serial.cpp:176-210
  *   tdg_scan             <- trussdec::scan(...)              truss_parallel.hpp:62, .cpp:21-37
  *   tdg_process_sublevel <- trussdec::process_sublevel(...)  truss_parallel.hpp:67-68, .cpp:39-104
  *
@@ -129,6 +130,15 @@ int tdg_build_truss_graph(tdg_context* ctx, const tdg_csr* g, uint32_t* eo, uint
 /* triangle_count (proj/src/triangle.cpp:90-116): number of triangles.
  * Host-pointer graph. */
 int tdg_triangle_count(tdg_context* ctx, const tdg_csr* g, uint64_t* count, tdg_times* times);
+
+/* ktruss_subgraphs (proj/src/truss_serial.cpp:176-210): the maximal
+ * k-trusses = connected components of the edges with truss >= k. truss[m] and
+ * comp_of_edge[m] are host arrays: comp_of_edge[e] = component index (components numbered
+ * in the order of their first edge id, as the reference returns them) or 0xFFFFFFFF for
+ * truss[e] < k; *ncomp = number of components. k < 2 or k > t_max (when t_max > 0) is
+ * TDG_ERR_INVALID (the reference's std::invalid_argument). */
+int tdg_ktruss_components(tdg_context* ctx, const tdg_csr* g, const uint32_t* truss, uint32_t k,
+                          uint32_t* comp_of_edge, uint64_t* ncomp);
 
 /* stats (host-pointer graph). */
 int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out);

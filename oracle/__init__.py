@@ -221,6 +221,8 @@ class Reference:
         L.ref_build_truss_graph.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p, _u32p, _u32p]
         L.ref_truss_wc.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p]
         L.ref_truss_oracle.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p]
+        L.ref_ktruss_components.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p, C.c_uint32, _u32p,
+                                            C.POINTER(C.c_uint64)]
         L.ref_triangle_count.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, C.c_int]
         L.ref_triangle_count.restype = C.c_int64
         L.ref_make_graph.argtypes = [C.c_int, C.c_int64, C.c_double, C.c_uint64, C.c_void_p, C.c_int64,
@@ -272,6 +274,18 @@ class Reference:
         t = np.zeros(max(g.m, 1), np.uint32)
         self._check(self.lib.ref_truss_oracle(g.n, g.m, g.offsets, g.neighbors, t))
         return t[: g.m]
+
+    def ktruss_subgraphs(self, g: Csr, truss, k: int) -> list[list[int]]:
+        """truss_serial.cpp:176-210 on the reference library; raises on invalid k."""
+        comp = np.zeros(max(g.m, 1), np.uint32)
+        nc = C.c_uint64()
+        tr = np.ascontiguousarray(truss, np.uint32) if g.m else np.zeros(1, np.uint32)
+        self._check(self.lib.ref_ktruss_components(g.n, g.m, g.offsets, g.neighbors, tr, k, comp, C.byref(nc)))
+        out = [[] for _ in range(nc.value)]
+        for e, c in enumerate(comp[: g.m].tolist()):
+            if c != 0xFFFFFFFF:
+                out[c].append(e)
+        return out
 
     def triangle_count(self, g: Csr, workers: int = 1) -> int:
         return int(self.lib.ref_triangle_count(g.n, g.m, g.offsets, g.neighbors, workers))

@@ -178,6 +178,24 @@ int64_t ref_triangle_count(int64_t n, int64_t m, const int64_t* off, const int32
     return out;
 }
 
+// ktruss_subgraphs (truss_serial.cpp:176-210) flattened to comp_out[e] = component index or
+// 0xFFFFFFFF; returns -1 with the reference's exception message on invalid k.
+int ref_ktruss_components(int64_t n, int64_t m, const int64_t* off, const int32_t* nb, const uint32_t* truss,
+                          uint32_t k, uint32_t* comp_out, uint64_t* ncomp) {
+    return guarded([&] {
+        TrussGraph tg = build_truss_graph(to_csr(n, m, off, nb));
+        TrussnessResult res;
+        res.truss.assign(truss, truss + m);
+        res.finalize();
+        auto comps = ktruss_subgraphs(tg, res, k);
+        for (int64_t e = 0; e < m; e++) comp_out[e] = 0xffffffffu;
+        for (size_t c = 0; c < comps.size(); c++)
+            for (EdgeId e : comps[c]) comp_out[e] = static_cast<uint32_t>(c);
+        *ncomp = comps.size();
+        return 0;
+    });
+}
+
 // Fixture graphs exactly as the reference tests build them (tests/helpers.hpp:12-43):
 // kind 0 = er_graph(n, p, seed), kind 1 = rmat_graph(scale=n, ef=(int)p, seed),
 // kind 2 = canonicalize(pairs). CSR written into caller buffers (capacities given).

@@ -538,6 +538,46 @@ int tdg_triangle_count(tdg_context* ctx, const tdg_csr* g, uint64_t* count, tdg_
     });
 }
 
+int tdg_ktruss_components(tdg_context* ctx, const tdg_csr* g, const uint32_t* truss, uint32_t k,
+                          uint32_t* comp_of_edge, uint64_t* ncomp) {
+    return guarded([&] {
+        if (!ncomp || (g && g->m && (!truss || !comp_of_edge))) throw Fail{TDG_ERR_INVALID, "NULL argument"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, true);
+        uint32_t t_max = 0;
+        for (uint32_t e = 0; e < d.m; e++) t_max = truss[e] > t_max ? truss[e] : t_max;
+        if (k < 2 || (t_max > 0 && k > t_max))  // truss_serial.cpp:179-180
+            throw Fail{TDG_ERR_INVALID, "ktruss_subgraphs: k out of range [2, t_max]"};
+        *ncomp = 0;
+        c->launches = 0;
+        stage_and_build(c, g, d, true, false, false);
+        if (d.m == 0) { ck(cudaStreamSynchronize(c->stream), "sync"); return; }
+        // scratch: s <- truss, stamp-buffer halves / lists for the rest
+        c->ensure_peel(d.n, d.m);
+        c->truss.ensure(size_t(d.m) * 4, "truss");
+        c->f0.ensure((size_t(d.m) + 1) * 4, "flag");
+        c->f1.ensure((size_t(d.m) + 1) * 4, "rank");
+        c->cub.ensure(ktruss_cub_bytes(d.m), "cub");
+        ck(cudaMemcpyAsync(c->truss.p, truss, size_t(d.m) * 4, cudaMemcpyHostToDevice, c->stream), "H2D truss");
+        KtrussBufs kb;
+        kb.parent = c->dl.as<uint32_t>();
+        kb.first = c->up.as<uint32_t>();
+        kb.root_of_edge = c->L0.as<uint32_t>();
+        kb.flag = c->f0.as<uint32_t>();
+        kb.rank = c->f1.as<uint32_t>();
+        kb.comp = c->L1.as<uint32_t>();
+        kb.cub_tmp = c->cub.p;
+        kb.cub_bytes = c->cub.cap;
+        ck(launch_ktruss(c->el.as<uint2>(), c->truss.as<uint32_t>(), d.n, d.m, k, kb, c->stream, &c->launches),
+           "ktruss kernels");
+        ck(cudaMemcpyAsync(comp_of_edge, kb.comp, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H comp");
+        ck(cudaMemcpyAsync(&c->hctl->htab_quads, kb.rank + d.m, 4, cudaMemcpyDeviceToHost, c->stream), "D2H ncomp");
+        ck(cudaStreamSynchronize(c->stream), "ktruss");
+        *ncomp = c->hctl->htab_quads;
+    });
+}
+
 int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out) {
     return guarded([&] {
         if (!out) throw Fail{TDG_ERR_INVALID, "out is NULL"};

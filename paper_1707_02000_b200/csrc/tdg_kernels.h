@@ -66,6 +66,21 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint32_t* ocnt, unsig
 cudaError_t launch_triangle_count(const DevGraph& g, unsigned long long* wpre, unsigned long long* bsum,
                                   SupportCtl* ctl, int sm_count, cudaStream_t st, uint32_t* launches);
 
+// ---- k-truss components (truss_serial.cpp:176-210) ----
+struct KtrussBufs {
+    uint32_t* parent;        // n
+    uint32_t* first;         // n: min qualifying edge id per root
+    uint32_t* root_of_edge;  // m
+    uint32_t* flag;          // m+1
+    uint32_t* rank;          // m+1 (rank[m] = number of components)
+    uint32_t* comp;          // m output
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+size_t ktruss_cub_bytes(uint32_t m);
+cudaError_t launch_ktruss(const uint2* el, const uint32_t* truss, uint32_t n, uint32_t m, uint32_t k,
+                          const KtrussBufs& b, cudaStream_t st, uint32_t* launches);
+
 // ---- peel (truss_parallel.cpp:21-150 equivalent) ----
 struct PhaseCtr {
     unsigned long long work; // sub-level: total probe items (informational)

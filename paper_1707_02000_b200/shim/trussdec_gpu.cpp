@@ -59,6 +59,26 @@ GraphStats stats(const CsrGraph& g) {
 
 SupportArray support_am4(const TrussGraph& tg, int workers) { return support_am4_as<SupportArray>(tg, workers); }
 
+std::uint64_t triangle_count(const TrussGraph& tg, int /*workers*/) {
+    std::vector<std::int64_t> off64;
+    const tdg_csr v = view(tg.csr, off64);
+    std::uint64_t c = 0;
+    check(tdg_triangle_count(default_context(), &v, &c, nullptr));
+    return c;
+}
+
+std::vector<std::vector<EdgeId>> ktruss_subgraphs(const TrussGraph& tg, const TrussnessResult& res, std::uint32_t k) {
+    std::vector<std::int64_t> off64;
+    const tdg_csr v = view(tg.csr, off64);
+    std::vector<std::uint32_t> comp(tg.csr.m + 1ull);
+    std::uint64_t nc = 0;
+    check(tdg_ktruss_components(default_context(), &v, res.truss.data(), k, comp.data(), &nc));
+    std::vector<std::vector<EdgeId>> out(nc);
+    for (std::uint32_t e = 0; e < tg.csr.m; e++)
+        if (comp[e] != 0xffffffffu) out[comp[e]].push_back(e);  // ascending edge ids per component
+    return out;
+}
+
 ParallelDecomposition truss_parallel(const TrussGraph& tg, int workers) {
     return truss_parallel_as<ParallelDecomposition>(tg, workers);
 }

@@ -172,6 +172,9 @@ SA support_am4_as(const TG& tg, int /*workers*/) {
 }
 
 // ---- reference-named entry points on the mirrored types ----
+std::uint64_t triangle_count(const TrussGraph& tg, int workers);  // triangle.hpp:19
+std::vector<std::vector<EdgeId>> ktruss_subgraphs(const TrussGraph& tg, const TrussnessResult& res,
+                                                  std::uint32_t k);  // truss_serial.hpp:43-45
 TrussGraph build_truss_graph(const CsrGraph& g);
 GraphStats stats(const CsrGraph& g);
 SupportArray support_am4(const TrussGraph& tg, int workers);

@@ -335,3 +335,22 @@ def process_sublevel(frontier: LevelFrontier, tg: TrussGraph | CsrGraph, s: np.n
     base = frontier.next_size
     frontier.next[base: base + ns.value] = out[: ns.value]
     frontier.next_size = base + ns.value
+
+
+def ktruss_subgraphs(tg: TrussGraph | CsrGraph, res: TrussnessResult | np.ndarray, k: int) -> list[list[int]]:
+    """truss_serial.cpp:176-210: the maximal k-trusses (connected components of the edges
+    with truss >= k) as lists of edge ids, in the reference's order (components by first
+    edge id, edges ascending). Computed on the GPU (tdg_ktruss_components)."""
+    g = tg.csr if isinstance(tg, TrussGraph) else tg
+    truss = np.ascontiguousarray(res.truss if isinstance(res, TrussnessResult) else res, dtype=np.uint32)
+    comp = np.zeros(max(g.m, 1), np.uint32)
+    nc = C.c_uint64()
+    v = g._view()
+    tr = truss if len(truss) else np.zeros(1, np.uint32)
+    _ck(_lib.tdg().tdg_ktruss_components(default_context().handle, C.byref(v), tr.ctypes.data, k,
+                                         comp.ctypes.data, C.byref(nc)))
+    comp = comp[: g.m]
+    sel = np.nonzero(comp != 0xFFFFFFFF)[0]
+    order = np.argsort(comp[sel], kind="stable")
+    groups = np.split(sel[order], np.cumsum(np.bincount(comp[sel], minlength=nc.value))[:-1]) if nc.value else []
+    return [grp.astype(np.int64).tolist() for grp in groups]
