@@ -39,5 +39,9 @@ def test_ktruss_matches_reference(td, oracle, ref, rec):
     c = build_fixture(oracle, rec)
     g = gpu_graph(c)
     res = td.truss_parallel(g).result
-    for k in sorted({2, 3, max(2, res.t_max // 2), res.t_max}):
+    for k in sorted(k for k in {2, 3, res.t_max // 2, res.t_max} if 2 <= k <= res.t_max):
         assert td.ktruss_subgraphs(g, res, k) == ref.ktruss_subgraphs(c, res.truss, k), (rec["name"], k)
+    with pytest.raises(ValueError):  # truss_serial.cpp:179-180 on both sides
+        td.ktruss_subgraphs(g, res, res.t_max + 1)
+    with pytest.raises(RuntimeError):
+        ref.ktruss_subgraphs(c, res.truss, res.t_max + 1)
