@@ -15,6 +15,8 @@
  *   tdg_stats            <- trussdec::stats(const CsrGraph&)  proj/src/graph.cpp:135-150
  *   tdg_triangle_count   <- trussdec::triangle_count(const TrussGraph&, int)  triangle.cpp:90-116
  *   tdg_ktruss_components<- trussdec::ktruss_subgraphs(tg, res, k)  truss_serial.cpp:176-210
+ *   tdg_kcore / tdg_coreness_order / tdg_reorder
+ *                        <- kcore_parallel / coreness_order (kcore.cpp:68-138), reorder (graph.cpp:103-133)
  *   tdg_scan             <- trussdec::scan(...)              truss_parallel.hpp:62, .cpp:21-37
  *   tdg_process_sublevel <- trussdec::process_sublevel(...)  truss_parallel.hpp:67-68, .cpp:39-104
  *
@@ -139,6 +141,20 @@ int tdg_triangle_count(tdg_context* ctx, const tdg_csr* g, uint64_t* count, tdg_
  * TDG_ERR_INVALID (the reference's std::invalid_argument). */
 int tdg_ktruss_components(tdg_context* ctx, const tdg_csr* g, const uint32_t* truss, uint32_t k,
                           uint32_t* comp_of_edge, uint64_t* ncomp);
+
+/* Vertex ordering before the path (the CLI's --reorder kcore pipeline,
+ * tools/trussdec.cpp:92-97):
+ *   tdg_kcore          <- kcore_parallel (proj/src/kcore.cpp:68-127): core_out[n], *c_max.
+ *   tdg_coreness_order <- coreness_order (kcore.cpp:129-138): perm_out[v] = new id, vertices
+ *                         stably sorted by (coreness, id).
+ *   tdg_reorder        <- reorder (proj/src/graph.cpp:103-133): relabel by perm and re-sort
+ *                         every list; out_offsets[n+1], out_neighbors[2m]. A perm that is not
+ *                         a bijection on 0..n-1 is TDG_ERR_INVALID (std::invalid_argument).
+ * All host pointers. */
+int tdg_kcore(tdg_context* ctx, const tdg_csr* g, uint32_t* core_out, uint32_t* c_max);
+int tdg_coreness_order(tdg_context* ctx, uint64_t n, const uint32_t* core, uint32_t* perm_out);
+int tdg_reorder(tdg_context* ctx, const tdg_csr* g, const uint32_t* perm, int64_t* out_offsets,
+                int32_t* out_neighbors);
 
 /* stats (host-pointer graph). */
 int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out);

@@ -223,6 +223,9 @@ class Reference:
         L.ref_truss_oracle.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p]
         L.ref_ktruss_components.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p, C.c_uint32, _u32p,
                                             C.POINTER(C.c_uint64)]
+        L.ref_kcore_order.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, C.c_int, _u32p, C.POINTER(C.c_uint32),
+                                      _u32p]
+        L.ref_reorder.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p, _i64p, _i32p]
         L.ref_triangle_count.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, C.c_int]
         L.ref_triangle_count.restype = C.c_int64
         L.ref_make_graph.argtypes = [C.c_int, C.c_int64, C.c_double, C.c_uint64, C.c_void_p, C.c_int64,
@@ -286,6 +289,21 @@ class Reference:
             if c != 0xFFFFFFFF:
                 out[c].append(e)
         return out
+
+    def kcore_order(self, g: Csr, workers: int = 1):
+        """kcore_parallel + coreness_order: (core[n], c_max, perm[n])."""
+        core = np.zeros(max(g.n, 1), np.uint32)
+        perm = np.zeros(max(g.n, 1), np.uint32)
+        cm = C.c_uint32()
+        self._check(self.lib.ref_kcore_order(g.n, g.m, g.offsets, g.neighbors, workers, core, C.byref(cm), perm))
+        return core[: g.n], cm.value, perm[: g.n]
+
+    def reorder(self, g: Csr, perm) -> Csr:
+        off = np.zeros(g.n + 1, np.int64)
+        nb = np.zeros(max(2 * g.m, 1), np.int32)
+        self._check(self.lib.ref_reorder(g.n, g.m, g.offsets, g.neighbors, np.ascontiguousarray(perm, np.uint32),
+                                         off, nb))
+        return Csr(g.n, g.m, off, nb[: 2 * g.m])
 
     def triangle_count(self, g: Csr, workers: int = 1) -> int:
         return int(self.lib.ref_triangle_count(g.n, g.m, g.offsets, g.neighbors, workers))

@@ -196,6 +196,29 @@ int ref_ktruss_components(int64_t n, int64_t m, const int64_t* off, const int32_
     });
 }
 
+// kcore_parallel + coreness_order (kcore.cpp:68-138) and reorder (graph.cpp:103-133).
+int ref_kcore_order(int64_t n, int64_t m, const int64_t* off, const int32_t* nb, int workers, uint32_t* core_out,
+                    uint32_t* c_max, uint32_t* perm_out) {
+    return guarded([&] {
+        CorenessResult r = kcore_parallel(to_csr(n, m, off, nb), workers);
+        std::memcpy(core_out, r.core.data(), static_cast<size_t>(n) * 4);
+        *c_max = r.c_max;
+        std::vector<VertexId> p = coreness_order(r);
+        std::memcpy(perm_out, p.data(), static_cast<size_t>(n) * 4);
+        return 0;
+    });
+}
+
+int ref_reorder(int64_t n, int64_t m, const int64_t* off, const int32_t* nb, const uint32_t* perm,
+                int64_t* off_out, int32_t* nb_out) {
+    return guarded([&] {
+        CsrGraph r = reorder(to_csr(n, m, off, nb), std::vector<VertexId>(perm, perm + n));
+        for (int64_t i = 0; i <= n; i++) off_out[i] = r.offsets[i];
+        std::memcpy(nb_out, r.neighbors.data(), static_cast<size_t>(2 * m) * 4);
+        return 0;
+    });
+}
+
 // Fixture graphs exactly as the reference tests build them (tests/helpers.hpp:12-43):
 // kind 0 = er_graph(n, p, seed), kind 1 = rmat_graph(scale=n, ef=(int)p, seed),
 // kind 2 = canonicalize(pairs). CSR written into caller buffers (capacities given).

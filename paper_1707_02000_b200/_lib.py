@@ -81,6 +81,9 @@ SIGNATURES = [
     ("tdg_stats", _i32, [_vp, _P(tdg_csr), _P(tdg_graph_stats)]),
     ("tdg_triangle_count", _i32, [_vp, _P(tdg_csr), _P(_u64), _P(tdg_times)]),
     ("tdg_ktruss_components", _i32, [_vp, _P(tdg_csr), _vp, _u32, _vp, _P(_u64)]),
+    ("tdg_kcore", _i32, [_vp, _P(tdg_csr), _vp, _P(_u32)]),
+    ("tdg_coreness_order", _i32, [_vp, _u64, _vp, _vp]),
+    ("tdg_reorder", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp]),
     ("tdg_scan", _i32, [_vp, _vp, _u64, _u32, _vp, _vp, _vp, _P(_u64)]),
     ("tdg_process_sublevel", _i32, [_vp, _P(tdg_csr), _vp, _u32, _vp, _u64, _vp, _vp, _vp, _vp, _P(_u64)]),
 ]

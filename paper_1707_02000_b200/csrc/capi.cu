@@ -76,6 +76,7 @@ struct tdg_context {
     cudaStream_t stream = nullptr;
     DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx;
     DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab, Ls, bhist, bcur, trace;
+    DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad;
     HostCtl* hctl = nullptr;
     cudaEvent_t ev[8] = {};
     uint32_t launches = 0;
@@ -198,8 +199,36 @@ struct tdg_context {
     void trim() {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
                          &osrc, &stask, &sx, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
-                         &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &Ls, &bhist, &bcur, &trace};
+                         &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &Ls, &bhist, &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1,
+                         &kwpre, &kctl, &ktmp, &knoff, &knadj, &kperm, &kbad};
         for (DevBuf* b : all) b->release();
+    }
+    KcoreBufs kcore_bufs(uint64_t n, uint64_t m) {
+        kdeg.ensure((n + 2) * 4, "kdeg");
+        kcore.ensure((n + 2) * 4, "kcore");
+        kL0.ensure(n * 4, "kL0");
+        kL1.ensure(n * 4, "kL1");
+        kA0.ensure(n * 4, "kA0");
+        kA1.ensure(n * 4, "kA1");
+        kwpre.ensure(n * 8, "kwpre");
+        kctl.ensure(kKcoreCtlBytes, "kctl");
+        ktmp.ensure(2 * m * 4, "ktmp");
+        bsum.ensure(sizeof(unsigned long long) * kMaxChunks, "bsum");
+        cub.ensure(kcore_cub_bytes(static_cast<uint32_t>(n), static_cast<uint32_t>(m)), "cub");
+        KcoreBufs b;
+        b.deg = kdeg.as<uint32_t>();
+        b.core = kcore.as<uint32_t>();
+        b.L0 = kL0.as<uint32_t>();
+        b.L1 = kL1.as<uint32_t>();
+        b.A0 = kA0.as<uint32_t>();
+        b.A1 = kA1.as<uint32_t>();
+        b.tmp_adj = ktmp.as<uint32_t>();
+        b.wpre = kwpre.as<unsigned long long>();
+        b.bsum = bsum.as<unsigned long long>();
+        b.ctl = kctl.p;
+        b.cub_tmp = cub.p;
+        b.cub_bytes = cub.cap;
+        return b;
     }
     float ms(int a, int b) const {
         float t = 0;
@@ -575,6 +604,76 @@ int tdg_ktruss_components(tdg_context* ctx, const tdg_csr* g, const uint32_t* tr
         ck(cudaMemcpyAsync(&c->hctl->htab_quads, kb.rank + d.m, 4, cudaMemcpyDeviceToHost, c->stream), "D2H ncomp");
         ck(cudaStreamSynchronize(c->stream), "ktruss");
         *ncomp = c->hctl->htab_quads;
+    });
+}
+
+int tdg_kcore(tdg_context* ctx, const tdg_csr* g, uint32_t* core_out, uint32_t* c_max) {
+    return guarded([&] {
+        if (!c_max || (g && g->n && !core_out)) throw Fail{TDG_ERR_INVALID, "NULL argument"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, true);
+        c->launches = 0;
+        *c_max = 0;
+        stage_and_build(c, g, d, true, false, false);
+        const KcoreBufs kb = c->kcore_bufs(d.n, d.m);
+        ck(launch_kcore(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), d.n, kb, c->sms, c->stream, &c->launches,
+                        kb.deg + d.n), "kcore kernel");
+        if (d.n) {
+            ck(cudaMemcpyAsync(core_out, kb.core, size_t(d.n) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H core");
+            ck(cudaMemcpyAsync(&c->hctl->htab_quads, kb.deg + d.n, 4, cudaMemcpyDeviceToHost, c->stream), "D2H c_max");
+        }
+        ck(cudaStreamSynchronize(c->stream), "kcore");
+        *c_max = d.n ? c->hctl->htab_quads : 0;
+    });
+}
+
+int tdg_coreness_order(tdg_context* ctx, uint64_t n, const uint32_t* core, uint32_t* perm_out) {
+    return guarded([&] {
+        if (n && (!core || !perm_out)) throw Fail{TDG_ERR_INVALID, "NULL argument"};
+        if (n >= 0xffffffffull) throw Fail{TDG_ERR_RANGE, "too many vertices"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        if (n == 0) return;
+        c->launches = 0;
+        const KcoreBufs kb = c->kcore_bufs(n, 0);
+        c->kperm.ensure(n * 4, "perm");
+        ck(cudaMemcpyAsync(kb.A0, core, n * 4, cudaMemcpyHostToDevice, c->stream), "H2D core");
+        // sort keys come from a copy so the caller's order array stays untouched
+        ck(cudaMemcpyAsync(kb.core, kb.A0, n * 4, cudaMemcpyDeviceToDevice, c->stream), "D2D core");
+        ck(launch_coreness_order(kb.core, static_cast<uint32_t>(n), kb, c->kperm.as<uint32_t>(), c->stream,
+                                 &c->launches), "coreness order");
+        ck(cudaMemcpyAsync(perm_out, c->kperm.p, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H perm");
+        ck(cudaStreamSynchronize(c->stream), "coreness order");
+    });
+}
+
+int tdg_reorder(tdg_context* ctx, const tdg_csr* g, const uint32_t* perm, int64_t* out_offsets,
+                int32_t* out_neighbors) {
+    return guarded([&] {
+        tdg_context* c = resolve(ctx);
+        c->use();
+        const Dims d = check_graph(g, true);
+        if (!out_offsets || (d.n && !perm) || (d.m && !out_neighbors)) throw Fail{TDG_ERR_INVALID, "NULL argument"};
+        c->launches = 0;
+        stage_and_build(c, g, d, true, false, false);
+        const KcoreBufs kb = c->kcore_bufs(d.n, d.m);
+        c->kperm.ensure((size_t(d.n) + 1) * 4, "perm");
+        c->knoff.ensure((size_t(d.n) + 1) * 4, "noff");
+        c->knadj.ensure(size_t(d.m) * 8, "nadj");
+        c->kbad.ensure(4, "bad");
+        if (d.n) ck(cudaMemcpyAsync(c->kperm.p, perm, size_t(d.n) * 4, cudaMemcpyHostToDevice, c->stream), "H2D perm");
+        ck(launch_reorder(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->kperm.as<uint32_t>(), d.n, d.m, kb,
+                          c->knoff.as<uint32_t>(), c->knadj.as<uint32_t>(), c->kbad.as<uint32_t>(), c->stream,
+                          &c->launches), "reorder");
+        ck(cudaMemcpyAsync(&c->hctl->htab_quads, c->kbad.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H check");
+        ck(cudaStreamSynchronize(c->stream), "reorder");
+        if (c->hctl->htab_quads)  // graph.cpp:106-113
+            throw Fail{TDG_ERR_INVALID, "reorder: permutation is not a bijection on 0..n-1"};
+        std::vector<uint32_t> noff(size_t(d.n) + 1);
+        ck(cudaMemcpy(noff.data(), c->knoff.p, noff.size() * 4, cudaMemcpyDeviceToHost), "D2H offsets");
+        for (size_t i = 0; i < noff.size(); i++) out_offsets[i] = noff[i];
+        if (d.m) ck(cudaMemcpy(out_neighbors, c->knadj.p, size_t(d.m) * 8, cudaMemcpyDeviceToHost), "D2H neighbors");
     });
 }
 

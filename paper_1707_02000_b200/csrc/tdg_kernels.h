@@ -81,6 +81,28 @@ size_t ktruss_cub_bytes(uint32_t m);
 cudaError_t launch_ktruss(const uint2* el, const uint32_t* truss, uint32_t n, uint32_t m, uint32_t k,
                           const KtrussBufs& b, cudaStream_t st, uint32_t* launches);
 
+// ---- vertex ordering (kcore.cpp:68-138, graph.cpp:103-133) ----
+struct KcoreBufs {
+    uint32_t* deg;            // n+1
+    uint32_t* core;           // n+1
+    uint32_t *L0, *L1, *A0, *A1;  // n each
+    uint32_t* tmp_adj;        // 2m (reorder)
+    unsigned long long* wpre;  // n
+    unsigned long long* bsum;  // kMaxChunks
+    void* ctl;                // device control block (kKcoreCtlBytes)
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+constexpr size_t kKcoreCtlBytes = 256;
+size_t kcore_cub_bytes(uint32_t n, uint32_t m);
+cudaError_t launch_kcore(const uint32_t* off, const uint32_t* adj, uint32_t n, const KcoreBufs& b, int sm_count,
+                         cudaStream_t st, uint32_t* launches, uint32_t* c_max_dev);
+cudaError_t launch_coreness_order(const uint32_t* core, uint32_t n, const KcoreBufs& b, uint32_t* perm,
+                                  cudaStream_t st, uint32_t* launches);
+cudaError_t launch_reorder(const uint32_t* off, const uint32_t* adj, const uint32_t* perm, uint32_t n, uint32_t m,
+                           const KcoreBufs& b, uint32_t* noff, uint32_t* nadj, uint32_t* bad, cudaStream_t st,
+                           uint32_t* launches);
+
 // ---- peel (truss_parallel.cpp:21-150 equivalent) ----
 struct PhaseCtr {
     unsigned long long work; // sub-level: total probe items (informational)

@@ -59,6 +59,40 @@ GraphStats stats(const CsrGraph& g) {
 
 SupportArray support_am4(const TrussGraph& tg, int workers) { return support_am4_as<SupportArray>(tg, workers); }
 
+CorenessResult kcore_parallel(const CsrGraph& g, int /*workers*/) {
+    std::vector<std::int64_t> off64;
+    const tdg_csr v = view(g, off64);
+    CorenessResult r;
+    r.core.assign(g.n, 0);
+    check(tdg_kcore(default_context(), &v, r.core.data(), &r.c_max));
+    return r;
+}
+
+std::vector<VertexId> coreness_order(const CorenessResult& res) {
+    std::vector<VertexId> perm(res.core.size());
+    check(tdg_coreness_order(default_context(), res.core.size(), res.core.data(), perm.data()));
+    return perm;
+}
+
+CsrGraph reorder(const CsrGraph& g, const std::vector<VertexId>& perm) {
+    if (perm.size() != g.n) throw std::invalid_argument("reorder: permutation size does not match vertex count");
+    std::vector<std::int64_t> off64;
+    const tdg_csr v = view(g, off64);
+    std::vector<std::int64_t> noff(g.n + 1ull);
+    CsrGraph out;
+    out.n = g.n;
+    out.m = g.m;
+    out.neighbors.resize(2ull * g.m);
+    check(tdg_reorder(default_context(), &v, perm.data(), noff.data(),
+                      reinterpret_cast<std::int32_t*>(out.neighbors.data())));
+    out.offsets.assign(noff.begin(), noff.end());
+    if (!g.labels.empty()) {
+        out.labels.resize(g.n);
+        for (VertexId u = 0; u < g.n; u++) out.labels[perm[u]] = g.labels[u];
+    }
+    return out;
+}
+
 std::uint64_t triangle_count(const TrussGraph& tg, int /*workers*/) {
     std::vector<std::int64_t> off64;
     const tdg_csr v = view(tg.csr, off64);

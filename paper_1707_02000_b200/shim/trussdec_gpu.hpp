@@ -171,7 +171,15 @@ SA support_am4_as(const TG& tg, int /*workers*/) {
     return s;
 }
 
+struct CorenessResult {  // kcore.hpp:9-12
+    std::vector<std::uint32_t> core;
+    std::uint32_t c_max = 0;
+};
+
 // ---- reference-named entry points on the mirrored types ----
+CorenessResult kcore_parallel(const CsrGraph& g, int workers);                    // kcore.hpp:19
+std::vector<VertexId> coreness_order(const CorenessResult& res);                   // kcore.hpp:23
+CsrGraph reorder(const CsrGraph& g, const std::vector<VertexId>& perm);            // graph.hpp:72
 std::uint64_t triangle_count(const TrussGraph& tg, int workers);  // triangle.hpp:19
 std::vector<std::vector<EdgeId>> ktruss_subgraphs(const TrussGraph& tg, const TrussnessResult& res,
                                                   std::uint32_t k);  // truss_serial.hpp:43-45

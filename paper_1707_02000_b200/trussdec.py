@@ -354,3 +354,46 @@ def ktruss_subgraphs(tg: TrussGraph | CsrGraph, res: TrussnessResult | np.ndarra
     order = np.argsort(comp[sel], kind="stable")
     groups = np.split(sel[order], np.cumsum(np.bincount(comp[sel], minlength=nc.value))[:-1]) if nc.value else []
     return [grp.astype(np.int64).tolist() for grp in groups]
+
+
+@dataclass
+class CorenessResult:
+    """kcore.hpp:9-12."""
+    core: np.ndarray
+    c_max: int = 0
+
+
+def kcore_parallel(g: CsrGraph, workers: int = 1) -> CorenessResult:
+    """kcore.cpp:68-127 on the GPU (tdg_kcore)."""
+    core = np.zeros(max(g.n, 1), np.uint32)
+    cmax = C.c_uint32()
+    v = g._view()
+    _ck(_lib.tdg().tdg_kcore(default_context().handle, C.byref(v), core.ctypes.data, C.byref(cmax)))
+    return CorenessResult(core[: g.n], cmax.value)
+
+
+def coreness_order(res: CorenessResult) -> np.ndarray:
+    """kcore.cpp:129-138: perm[v] = new id (stable by (coreness, id)), on the GPU."""
+    core = np.ascontiguousarray(res.core, np.uint32)
+    n = len(core)
+    perm = np.zeros(max(n, 1), np.uint32)
+    _ck(_lib.tdg().tdg_coreness_order(default_context().handle, n, core.ctypes.data if n else None,
+                                      perm.ctypes.data))
+    return perm[:n]
+
+
+def reorder(g: CsrGraph, perm) -> CsrGraph:
+    """graph.cpp:103-133: relabel vertex v as perm[v] and re-sort every adjacency list."""
+    p = np.ascontiguousarray(perm, np.uint32)
+    if len(p) != g.n:
+        raise ValueError("reorder: permutation size does not match vertex count")
+    off = np.zeros(g.n + 1, np.int64)
+    nb = np.zeros(max(2 * g.m, 1), np.int32)
+    v = g._view()
+    pp = p if len(p) else np.zeros(1, np.uint32)
+    _ck(_lib.tdg().tdg_reorder(default_context().handle, C.byref(v), pp.ctypes.data, off.ctypes.data, nb.ctypes.data))
+    labels = None
+    if g.labels is not None:
+        labels = np.empty_like(g.labels)
+        labels[p] = g.labels
+    return CsrGraph(g.n, g.m, off, nb[: 2 * g.m], labels)
