@@ -15,6 +15,7 @@
  *   tdg_stats            <- trussdec::stats(const CsrGraph&)  proj/src/graph.cpp:135-150
  *   tdg_triangle_count   <- trussdec::triangle_count(const TrussGraph&, int)  triangle.cpp:90-116
  *   tdg_ktruss_components<- trussdec::ktruss_subgraphs(tg, res, k)  truss_serial.cpp:176-210
+ *   tdg_canonicalize     <- trussdec::canonicalize(const RawEdgeList&)  graph.cpp:19-71
  *   tdg_kcore / tdg_coreness_order / tdg_reorder
  *                        <- kcore_parallel / coreness_order (kcore.cpp:68-138), reorder (graph.cpp:103-133)
  *   tdg_scan             <- trussdec::scan(...)              truss_parallel.hpp:62, .cpp:21-37
@@ -155,6 +156,14 @@ int tdg_kcore(tdg_context* ctx, const tdg_csr* g, uint32_t* core_out, uint32_t* 
 int tdg_coreness_order(tdg_context* ctx, uint64_t n, const uint32_t* core, uint32_t* perm_out);
 int tdg_reorder(tdg_context* ctx, const tdg_csr* g, const uint32_t* perm, int64_t* out_offsets,
                 int32_t* out_neighbors);
+
+/* Ingest <- canonicalize (proj/src/graph.cpp:19-71): pairs[2*npairs] raw
+ * labels (duplicates, both orientations, self loops allowed). Labels get dense ids in
+ * first-appearance order (a then b per pair), loops are dropped, pairs deduplicated; the
+ * CSR is written to offsets[n+1], neighbors[2m], labels[n] (original label of every id).
+ * Capacities: offsets 2*npairs+1, neighbors 2*npairs, labels 2*npairs. Host pointers. */
+int tdg_canonicalize(tdg_context* ctx, const uint64_t* pairs, uint64_t npairs, int64_t* offsets,
+                     int32_t* neighbors, uint64_t* labels, int64_t* n_out, int64_t* m_out);
 
 /* stats (host-pointer graph). */
 int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out);

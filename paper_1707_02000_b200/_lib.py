@@ -84,6 +84,7 @@ SIGNATURES = [
     ("tdg_kcore", _i32, [_vp, _P(tdg_csr), _vp, _P(_u32)]),
     ("tdg_coreness_order", _i32, [_vp, _u64, _vp, _vp]),
     ("tdg_reorder", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp]),
+    ("tdg_canonicalize", _i32, [_vp, _vp, _u64, _vp, _vp, _vp, _P(C.c_int64), _P(C.c_int64)]),
     ("tdg_scan", _i32, [_vp, _vp, _u64, _u32, _vp, _vp, _vp, _P(_u64)]),
     ("tdg_process_sublevel", _i32, [_vp, _P(tdg_csr), _vp, _u32, _vp, _u64, _vp, _vp, _vp, _vp, _P(_u64)]),
 ]

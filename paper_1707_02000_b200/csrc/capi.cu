@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstdint>
 #include <mutex>
 #include <new>
 #include <string>
@@ -76,7 +77,7 @@ struct tdg_context {
     cudaStream_t stream = nullptr;
     DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx;
     DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab, Ls, bhist, bcur, trace;
-    DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad;
+    DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing;
     HostCtl* hctl = nullptr;
     cudaEvent_t ev[8] = {};
     uint32_t launches = 0;
@@ -200,7 +201,7 @@ struct tdg_context {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
                          &osrc, &stask, &sx, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
                          &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &Ls, &bhist, &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1,
-                         &kwpre, &kctl, &ktmp, &knoff, &knadj, &kperm, &kbad};
+                         &kwpre, &kctl, &ktmp, &knoff, &knadj, &kperm, &kbad, &ing};
         for (DevBuf* b : all) b->release();
     }
     KcoreBufs kcore_bufs(uint64_t n, uint64_t m) {
@@ -674,6 +675,67 @@ int tdg_reorder(tdg_context* ctx, const tdg_csr* g, const uint32_t* perm, int64_
         ck(cudaMemcpy(noff.data(), c->knoff.p, noff.size() * 4, cudaMemcpyDeviceToHost), "D2H offsets");
         for (size_t i = 0; i < noff.size(); i++) out_offsets[i] = noff[i];
         if (d.m) ck(cudaMemcpy(out_neighbors, c->knadj.p, size_t(d.m) * 8, cudaMemcpyDeviceToHost), "D2H neighbors");
+    });
+}
+
+int tdg_canonicalize(tdg_context* ctx, const uint64_t* pairs, uint64_t npairs, int64_t* offsets, int32_t* neighbors,
+                     uint64_t* labels, int64_t* n_out, int64_t* m_out) {
+    return guarded([&] {
+        if (!n_out || !m_out || !offsets || (npairs && (!pairs || !neighbors || !labels)))
+            throw Fail{TDG_ERR_INVALID, "NULL argument"};
+        if (2 * npairs >= 0xffffffffull)  // graph.cpp:30-31, 48-49 (32-bit ids and slots)
+            throw Fail{TDG_ERR_RANGE, "graph exceeds 32-bit edge width (2m too large)"};
+        tdg_context* c = resolve(ctx);
+        c->use();
+        *n_out = 0;
+        *m_out = 0;
+        offsets[0] = 0;
+        if (npairs == 0) return;
+        const uint64_t N = 2 * npairs;
+        // carve one allocation (8-byte arrays first)
+        const size_t cubb = ingest_cub_bytes(npairs);
+        const size_t bytes = 8 * (N * 4 + 2 * npairs + 1) + 4 * (N * 14 + 8) + cubb + 256;
+        c->ing.ensure(bytes, "ingest");
+        char* p = static_cast<char*>(c->ing.p);
+        auto take8 = [&](uint64_t cnt) { auto* r = reinterpret_cast<unsigned long long*>(p); p += 8 * cnt; return r; };
+        auto take4 = [&](uint64_t cnt) { auto* r = reinterpret_cast<uint32_t*>(p); p += 4 * cnt; return r; };
+        IngestBufs B;
+        B.labels_in = take8(N);
+        B.key_sorted = take8(N);
+        B.glabel = take8(N);
+        B.labels_out = take8(N);
+        B.keys = take8(npairs);
+        B.keys_sorted = take8(npairs);
+        B.nuniq = take8(1);
+        B.pos_in = take4(N);
+        B.pos_sorted = take4(N);
+        B.head = take4(N + 1);
+        B.gidx = take4(N + 1);
+        B.first_pos = take4(N);
+        B.gseq = take4(N);
+        B.first_sorted = take4(N);
+        B.gsorted = take4(N);
+        B.rank_of = take4(N);
+        B.vid = take4(N);
+        B.deg = take4(N + 1);
+        B.off = take4(N + 1);
+        B.cursor = take4(N + 1);
+        B.nb_tmp = take4(N);
+        B.nb = take4(N);
+        p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+        B.cub_tmp = p;
+        B.cub_bytes = cubb;
+        c->launches = 0;
+        ck(cudaMemcpyAsync(B.labels_in, pairs, N * 8, cudaMemcpyHostToDevice, c->stream), "H2D pairs");
+        uint64_t n = 0, m = 0;
+        ck(launch_ingest(B, npairs, c->stream, &n, &m, &c->launches), "ingest kernels");
+        std::vector<uint32_t> off(n + 1);
+        ck(cudaMemcpy(off.data(), B.off, (n + 1) * 4, cudaMemcpyDeviceToHost), "D2H offsets");
+        for (uint64_t i = 0; i <= n; i++) offsets[i] = off[i];
+        if (m) ck(cudaMemcpy(neighbors, B.nb, 2 * m * 4, cudaMemcpyDeviceToHost), "D2H neighbors");
+        ck(cudaMemcpy(labels, B.labels_out, n * 8, cudaMemcpyDeviceToHost), "D2H labels");
+        *n_out = static_cast<int64_t>(n);
+        *m_out = static_cast<int64_t>(m);
     });
 }
 

@@ -103,6 +103,19 @@ cudaError_t launch_reorder(const uint32_t* off, const uint32_t* adj, const uint3
                            const KcoreBufs& b, uint32_t* noff, uint32_t* nadj, uint32_t* bad, cudaStream_t st,
                            uint32_t* launches);
 
+// ---- ingest (graph.cpp:19-71 canonicalize) ----
+struct IngestBufs {
+    unsigned long long *labels_in, *key_sorted, *glabel, *labels_out, *keys, *keys_sorted, *nuniq;
+    uint32_t *pos_in, *pos_sorted, *head, *gidx, *first_pos, *gseq, *first_sorted, *gsorted, *rank_of, *vid;
+    uint32_t *deg, *off, *cursor, *nb_tmp, *nb;
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+size_t ingest_cub_bytes(uint64_t npairs);
+// Synchronises the stream (sizes are read back). *n_out distinct labels, *m_out edges.
+cudaError_t launch_ingest(const IngestBufs& B, uint64_t npairs, cudaStream_t st, uint64_t* n_out, uint64_t* m_out,
+                          uint32_t* launches);
+
 // ---- peel (truss_parallel.cpp:21-150 equivalent) ----
 struct PhaseCtr {
     unsigned long long work; // sub-level: total probe items (informational)

@@ -397,3 +397,18 @@ def reorder(g: CsrGraph, perm) -> CsrGraph:
         labels = np.empty_like(g.labels)
         labels[p] = g.labels
     return CsrGraph(g.n, g.m, off, nb[: 2 * g.m], labels)
+
+
+def canonicalize(pairs) -> CsrGraph:
+    """graph.cpp:19-71 on the GPU (tdg_canonicalize): raw label pairs -> CsrGraph with dense
+    ids in first-appearance order, loops dropped, duplicates merged, labels kept."""
+    raw = np.ascontiguousarray(np.asarray(pairs, dtype=np.uint64).reshape(-1))
+    k = len(raw) // 2
+    off = np.zeros(2 * k + 2, np.int64)
+    nb = np.zeros(max(2 * k, 1), np.int32)
+    lab = np.zeros(max(2 * k, 1), np.uint64)
+    n, m = C.c_int64(), C.c_int64()
+    rp = raw if len(raw) else np.zeros(2, np.uint64)
+    _ck(_lib.tdg().tdg_canonicalize(default_context().handle, rp.ctypes.data, k, off.ctypes.data, nb.ctypes.data,
+                                    lab.ctypes.data, C.byref(n), C.byref(m)))
+    return CsrGraph(n.value, m.value, off[: n.value + 1].copy(), nb[: 2 * m.value].copy(), lab[: n.value].copy())
