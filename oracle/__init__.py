@@ -310,6 +310,9 @@ class Reference:
 
     def make_graph(self, kind: int, a: int, b: float, seed: int, pairs=None) -> Csr:
         cap_n, cap_nb = 1 << 20, 1 << 24
+        if pairs is not None:
+            cap_n = max(cap_n, 2 * len(pairs) + 1)
+            cap_nb = max(cap_nb, 2 * len(pairs))
         off = np.zeros(cap_n + 1, np.int64)
         nb = np.zeros(cap_nb, np.int32)
         n, m = C.c_int64(), C.c_int64()

@@ -18,6 +18,7 @@
 #include "tdg_kernels.h"
 
 using namespace tdg;
+namespace tdg { extern const char* g_ingest_step; }
 
 namespace {
 
@@ -34,6 +35,13 @@ void ck(cudaError_t e, const char* what) {
         throw Fail{e == cudaErrorMemoryAllocation ? TDG_ERR_NOMEM : TDG_ERR_CUDA,
                     std::string(what) + ": " + cudaGetErrorString(e)};
     }
+}
+
+// Device->host copy ordered on the context's (non-blocking) stream, then waited for. A
+// plain cudaMemcpy runs on the legacy stream and would not wait for work queued on it.
+void d2h(cudaStream_t st, void* dst, const void* src, size_t bytes, const char* what) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), what);
+    ck(cudaStreamSynchronize(st), what);
 }
 
 struct DevBuf {
@@ -120,7 +128,7 @@ struct tdg_context {
         Ls.ensure(m * 4, "Ls");
         if (bhist.cap == 0) {
             bhist.ensure(kBuckets * 4, "bhist");
-            ck(cudaMemset(bhist.p, 0, kBuckets * 4), "memset");
+            ck(cudaMemsetAsync(bhist.p, 0, kBuckets * 4, stream), "memset");
         }
         bcur.ensure(kBuckets * 4, "bcur");
         nsl.ensure((n + 2) * 4, "nsl");
@@ -407,7 +415,7 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         if (const char* tp = std::getenv("TDG_TRACE")) {  // diagnostic dump: level, cs, W, ns, K
             const size_t k = std::min<size_t>(pc.sublevels, c->trace.cap / 32);
             std::vector<unsigned long long> h(4 * k);
-            if (k) ck(cudaMemcpy(h.data(), c->trace.p, 32 * k, cudaMemcpyDeviceToHost), "D2H trace");
+            if (k) d2h(c->stream, h.data(), c->trace.p, 32 * k, "D2H trace");
             if (FILE* f = std::fopen(tp, "w")) {
                 for (size_t i = 0; i < k; i++)
                     std::fprintf(f, "%llu %llu %llu %llu %llu\n", h[4 * i] >> 32, h[4 * i] & 0xffffffffull, h[4 * i + 1],
@@ -418,7 +426,7 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         if (nsl_len) *nsl_len = len;
         if (nsl_out && len) {
             const uint64_t k = len < nsl_cap ? len : nsl_cap;
-            if (k) ck(cudaMemcpy(nsl_out, pb.nsl, k * 4, cudaMemcpyDeviceToHost), "D2H nsl");
+            if (k) d2h(c->stream, nsl_out, pb.nsl, k * 4, "D2H nsl");
         }
         if (times) {
             fill_times(times, c, host, true);
@@ -672,9 +680,9 @@ int tdg_reorder(tdg_context* ctx, const tdg_csr* g, const uint32_t* perm, int64_
         if (c->hctl->htab_quads)  // graph.cpp:106-113
             throw Fail{TDG_ERR_INVALID, "reorder: permutation is not a bijection on 0..n-1"};
         std::vector<uint32_t> noff(size_t(d.n) + 1);
-        ck(cudaMemcpy(noff.data(), c->knoff.p, noff.size() * 4, cudaMemcpyDeviceToHost), "D2H offsets");
+        d2h(c->stream, noff.data(), c->knoff.p, noff.size() * 4, "D2H offsets");
         for (size_t i = 0; i < noff.size(); i++) out_offsets[i] = noff[i];
-        if (d.m) ck(cudaMemcpy(out_neighbors, c->knadj.p, size_t(d.m) * 8, cudaMemcpyDeviceToHost), "D2H neighbors");
+        if (d.m) d2h(c->stream, out_neighbors, c->knadj.p, size_t(d.m) * 8, "D2H neighbors");
     });
 }
 
@@ -694,7 +702,7 @@ int tdg_canonicalize(tdg_context* ctx, const uint64_t* pairs, uint64_t npairs, i
         const uint64_t N = 2 * npairs;
         // carve one allocation (8-byte arrays first)
         const size_t cubb = ingest_cub_bytes(npairs);
-        const size_t bytes = 8 * (N * 4 + 2 * npairs + 1) + 4 * (N * 14 + 8) + cubb + 256;
+        const size_t bytes = 8 * (N * 4 + 2 * npairs + 1) + 4 * (N * 15 + 8) + cubb + 256;
         c->ing.ensure(bytes, "ingest");
         char* p = static_cast<char*>(c->ing.p);
         auto take8 = [&](uint64_t cnt) { auto* r = reinterpret_cast<unsigned long long*>(p); p += 8 * cnt; return r; };
@@ -728,12 +736,15 @@ int tdg_canonicalize(tdg_context* ctx, const uint64_t* pairs, uint64_t npairs, i
         c->launches = 0;
         ck(cudaMemcpyAsync(B.labels_in, pairs, N * 8, cudaMemcpyHostToDevice, c->stream), "H2D pairs");
         uint64_t n = 0, m = 0;
-        ck(launch_ingest(B, npairs, c->stream, &n, &m, &c->launches), "ingest kernels");
+        {
+            const cudaError_t e = launch_ingest(B, npairs, c->stream, &n, &m, &c->launches);
+            ck(e, (std::string("ingest kernels after step '") + g_ingest_step + "'").c_str());
+        }
         std::vector<uint32_t> off(n + 1);
-        ck(cudaMemcpy(off.data(), B.off, (n + 1) * 4, cudaMemcpyDeviceToHost), "D2H offsets");
+        d2h(c->stream, off.data(), B.off, (n + 1) * 4, "D2H offsets");
         for (uint64_t i = 0; i <= n; i++) offsets[i] = off[i];
-        if (m) ck(cudaMemcpy(neighbors, B.nb, 2 * m * 4, cudaMemcpyDeviceToHost), "D2H neighbors");
-        ck(cudaMemcpy(labels, B.labels_out, n * 8, cudaMemcpyDeviceToHost), "D2H labels");
+        if (m) d2h(c->stream, neighbors, B.nb, 2 * m * 4, "D2H neighbors");
+        d2h(c->stream, labels, B.labels_out, n * 8, "D2H labels");
         *n_out = static_cast<int64_t>(n);
         *m_out = static_cast<int64_t>(m);
     });
@@ -794,7 +805,7 @@ int tdg_scan(tdg_context* ctx, const uint32_t* s, uint64_t m, uint32_t level, co
         ck(cudaMemcpyAsync(in_curr, c->f1.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H in_curr");
         ck(cudaStreamSynchronize(c->stream), "scan");
         const uint32_t cs = c->hctl->peel.ph[0].out_size;
-        if (cs) ck(cudaMemcpy(curr, pb.L[0], size_t(cs) * 4, cudaMemcpyDeviceToHost), "D2H curr");
+        if (cs) d2h(c->stream, curr, pb.L[0], size_t(cs) * 4, "D2H curr");
         *curr_size = cs;
     });
 }
@@ -836,7 +847,7 @@ int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32
         ck(cudaStreamSynchronize(c->stream), "process_sublevel");
         if (c->hctl->peel.overflow) throw Fail{TDG_ERR_RANGE, "work queue exceeded 32-bit piece counter"};
         const uint32_t ns = c->hctl->peel.ph[1].out_size;
-        if (ns) ck(cudaMemcpy(next, pb.L[1], size_t(ns) * 4, cudaMemcpyDeviceToHost), "D2H next");
+        if (ns) d2h(c->stream, next, pb.L[1], size_t(ns) * 4, "D2H next");
         *next_size = ns;
     });
 }

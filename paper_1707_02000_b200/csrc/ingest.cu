@@ -104,6 +104,8 @@ __global__ void k_fill(const unsigned long long* __restrict__ keys, const unsign
 
 }  // namespace
 
+const char* g_ingest_step = "";
+
 size_t ingest_cub_bytes(uint64_t npairs) {
     const uint64_t N = 2 * npairs > 0 ? 2 * npairs : 1;
     size_t a = 0, b = 0, c = 0, d = 0, e = 0;
@@ -132,12 +134,17 @@ cudaError_t launch_ingest(const IngestBufs& B, uint64_t npairs, cudaStream_t st,
     *n_out = 0;
     *m_out = 0;
     if (npairs == 0) return cudaSuccess;
+// launch-error check per step (no sync); the name tells the caller where a failure surfaced
+#define STEP(name) do { g_ingest_step = name; if ((err = cudaGetLastError()) != cudaSuccess) return err; } while (0)
     k_iota_u32<<<gfor(N), kT, 0, st>>>(B.pos_in, N);
+    STEP("iota");
     tmp = B.cub_bytes;
     if ((err = cub::DeviceRadixSort::SortPairs(B.cub_tmp, tmp, B.labels_in, B.key_sorted, B.pos_in, B.pos_sorted, N, 0,
                                                64, st)) != cudaSuccess)
         return err;
+    STEP("sort labels");
     k_heads<<<gfor(N + 1), kT, 0, st>>>(B.key_sorted, N, B.head);
+    STEP("heads");
     tmp = B.cub_bytes;
     if ((err = cub::DeviceScan::ExclusiveSum(B.cub_tmp, tmp, B.head, B.gidx, N + 1, st)) != cudaSuccess) return err;
     uint32_t ng = 0;
@@ -148,15 +155,20 @@ cudaError_t launch_ingest(const IngestBufs& B, uint64_t npairs, cudaStream_t st,
     if ((err = cub::DeviceRadixSort::SortPairs(B.cub_tmp, tmp, B.first_pos, B.first_sorted, B.gseq, B.gsorted, ng, 0,
                                                32, st)) != cudaSuccess)
         return err;
+    STEP("sort groups");
     k_rank<<<gfor(ng), kT, 0, st>>>(B.gsorted, B.glabel, ng, B.rank_of, B.labels_out);
+    STEP("rank");
     k_ids<<<gfor(N), kT, 0, st>>>(B.pos_sorted, B.gidx, B.rank_of, N, B.vid);
+    STEP("ids");
     k_keys<<<gfor(npairs), kT, 0, st>>>(B.vid, npairs, B.keys);
+    STEP("keys");
     tmp = B.cub_bytes;
     if ((err = cub::DeviceRadixSort::SortKeys(B.cub_tmp, tmp, B.keys, B.keys_sorted, npairs, 0, 64, st)) != cudaSuccess)
         return err;
     tmp = B.cub_bytes;
     if ((err = cub::DeviceSelect::Unique(B.cub_tmp, tmp, B.keys_sorted, B.keys, B.nuniq, npairs, st)) != cudaSuccess)
         return err;
+    STEP("unique");
     if ((err = cudaMemsetAsync(B.deg, 0, (uint64_t(ng) + 1) * 4, st)) != cudaSuccess) return err;
     k_degrees<<<gfor(npairs), kT, 0, st>>>(B.keys, B.nuniq, B.deg);
     tmp = B.cub_bytes;
@@ -164,7 +176,9 @@ cudaError_t launch_ingest(const IngestBufs& B, uint64_t npairs, cudaStream_t st,
         return err;
     if ((err = cudaMemcpyAsync(B.cursor, B.off, uint64_t(ng) * 4 + 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
         return err;
+    STEP("degrees");
     k_fill<<<gfor(npairs), kT, 0, st>>>(B.keys, B.nuniq, B.cursor, B.nb_tmp);
+    STEP("fill");
     uint32_t slots = 0;
     if ((err = cudaMemcpyAsync(&slots, B.off + ng, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return err;
     if ((err = cudaStreamSynchronize(st)) != cudaSuccess) return err;
