@@ -208,18 +208,38 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
             }
             const uint32_t relk = st <= base ? 0u
                                   : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
-            const uint32_t own = warp_search_le(relk, lane);
-            const unsigned long long so = shfl64(st, own);
-            const ITask ko = shfl_task(k, own);
-            const unsigned long long x = base + lane;
-            uint32_t ja = 0, e = kNone;
-            const bool active = x < limit;
-            if (active) {
-                ja = static_cast<uint32_t>(x - so);
-                e = P.find(ko, P.elems[ko.oa + ja]);
+            constexpr int U = Policy::kUnroll;
+            if constexpr (U > 1) {
+                // U items per lane per step (item base + lane + 32q): the policy issues their
+                // independent loads together, so each lane keeps U probe chains in flight.
+                ITask ko[U];
+                uint32_t ja[U];
+                bool act[U];
+#pragma unroll
+                for (int q = 0; q < U; q++) {
+                    const uint32_t key = lane + 32u * q;
+                    const uint32_t own = warp_search_le(relk, key);
+                    const unsigned long long so = shfl64(st, own);
+                    ko[q] = shfl_task(k, own);
+                    const unsigned long long x = base + key;
+                    act[q] = x < limit;
+                    ja[q] = act[q] ? static_cast<uint32_t>(x - so) : 0u;
+                }
+                P.template run<U>(act, ko, ja);
+            } else {
+                const uint32_t own = warp_search_le(relk, lane);
+                const unsigned long long so = shfl64(st, own);
+                const ITask ko = shfl_task(k, own);
+                const unsigned long long x = base + lane;
+                uint32_t ja = 0, e = kNone;
+                const bool active = x < limit;
+                if (active) {
+                    ja = static_cast<uint32_t>(x - so);
+                    e = P.find(ko, P.elems[ko.oa + ja]);
+                }
+                P.visit(active, e != kNone, ko, ja, e);
             }
-            P.visit(active, e != kNone, ko, ja, e);
-            const unsigned long long nb = base + 32 < limit ? base + 32 : limit;
+            const unsigned long long nb = base + 32u * U < limit ? base + 32u * U : limit;
             i = (nb >= end_held) ? i + 32 : i + warp_search_le(relk, static_cast<uint32_t>(nb - base));
             base = nb;
         }

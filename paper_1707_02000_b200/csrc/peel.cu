@@ -49,7 +49,10 @@ namespace {
 
 constexpr int kPeelThreads = 256;
 #ifndef TDG_PEEL_MINB
-#define TDG_PEEL_MINB 5  // min resident blocks/SM: 48 registers, 40 warps per SM
+#define TDG_PEEL_MINB 4  // min resident blocks/SM: 64 registers, 32 warps per SM
+#endif
+#ifndef TDG_PEEL_U
+#define TDG_PEEL_U 2  // probe items per lane per window step (independent chains in flight)
 #endif
 constexpr int kScanItems = 8;
 constexpr int kWarps = kPeelThreads / 32;
@@ -61,7 +64,7 @@ constexpr int kWarps = kPeelThreads / 32;
 //    the piece's slice of N(b) is staged in shared memory and searched there (PeelPolicy).
 constexpr uint32_t kStaged = 0x80000000u;
 #ifndef TDG_STAGE_MIN
-#define TDG_STAGE_MIN 128  // probe-list length from which a task may be staged
+#define TDG_STAGE_MIN 512  // probe-list length from which a task may be staged
 #endif
 #ifndef TDG_STAGE_RATIO
 #define TDG_STAGE_RATIO 8  // ... if the searched list is at most this many times longer
@@ -139,6 +142,28 @@ __device__ __forceinline__ void emit(uint32_t o0, uint32_t o1, PhaseCtr* out, ui
     if (o1 != kNone) next[p1] = o1;
 }
 
+// Append every lane's valid targets (o[j] != kNone) to next with one atomic per warp.
+template <int N>
+__device__ __forceinline__ void emit_many(const uint32_t (&o)[N], PhaseCtr* out, uint32_t* next) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < N; j++) c += o[j] != kNone ? 1u : 0u;
+    if (!__any_sync(kFull, c != 0)) return;
+    const uint32_t lane = lane_id();
+    uint32_t incl = c;
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += t;
+    }
+    uint32_t base = 0;
+    if (lane == 31) base = atomicAdd(&out->out_size, incl);
+    base = __shfl_sync(kFull, base, 31) + incl - c;
+#pragma unroll
+    for (int j = 0; j < N; j++)
+        if (o[j] != kNone) next[base++] = o[j];
+}
+
 // process_sublevel's inner loop (truss_parallel.cpp:80-88) as a probe-engine policy: a hit
 // is w in N(u) ∩ N(v): slot ja of the probe list (its eid is one peer) found in the other
 // endpoint's hash table (whose value is the other peer's id).
@@ -153,8 +178,104 @@ struct PeelPolicy {
     unsigned long long* hit_ctr;  // diagnostic, may be null
     uint32_t* stage;              // this warp's kStageB-entry shared buffer
     static constexpr bool kHasStaged = true;
+    static constexpr int kUnroll = TDG_PEEL_U;
     __device__ ITask load(uint32_t t) const { return ptask(g, curr[t]); }
     __device__ bool staged(const ITask& k) const { return (k.lb & kStaged) != 0; }
+    // U hash-form probes per lane, stage by stage so the U chains' loads overlap:
+    // list element + its edge id (coalesced) -> first table slot -> (collisions) ->
+    // both peers' state words -> both decrements -> one warp append for all targets.
+    template <int U>
+    __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
+        uint32_t x[U], ea[U], eb[U], h[U];
+        unsigned long long ent[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            x[q] = kHEmpty;
+            ea[q] = kNone;
+            if (act[q]) {
+                x[q] = elems[ko[q].oa + ja[q]];
+                ea[q] = g.eid[ko[q].oa + ja[q]];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            ent[q] = kHEmpty;
+            h[q] = 0;
+            if (act[q] && x[q] != ko[q].aux) {
+                h[q] = hmix(x[q]) & ko[q].lb;
+                ent[q] = g.htab[4ull * ko[q].ob + h[q]];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            unsigned long long e = ent[q];
+            uint32_t hh = h[q];
+            while (static_cast<uint32_t>(e) != kHEmpty && static_cast<uint32_t>(e) != x[q]) {
+                hh = (hh + 1) & ko[q].lb;
+                e = g.htab[4ull * ko[q].ob + hh];
+            }
+            eb[q] = (x[q] != kHEmpty && static_cast<uint32_t>(e) == x[q]) ? (static_cast<uint32_t>(e >> 32) & ~kHUp)
+                                                                           : kNone;
+        }
+        unsigned long long wa[U], wb[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            wa[q] = 0;
+            wb[q] = 0;
+            if (eb[q] != kNone) {
+                wa[q] = ld_state(ss, ea[q]);
+                wb[q] = ld_state(ss, eb[q]);
+            }
+        }
+        // try_dec (truss_parallel.cpp:49-63) split so all atomics issue before any result is used
+        uint32_t tg[2 * U], pv[2 * U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            tg[2 * q] = kNone;
+            tg[2 * q + 1] = kNone;
+            if (eb[q] != kNone) {
+                const uint32_t sa = st_stamp(wa[q]), sb = st_stamp(wb[q]);
+                if (!((sa != 0 && sa < K) || (sb != 0 && sb < K))) {  // :85 processed peer
+                    const uint32_t id = ko[q].id;
+                    if (st_s(wa[q]) > level && !(sb == K && id >= eb[q])) tg[2 * q] = ea[q];      // :86, :52-53
+                    if (st_s(wb[q]) > level && !(sa == K && id >= ea[q])) tg[2 * q + 1] = eb[q];  // :87
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 2 * U; j++)
+            if (tg[j] != kNone) pv[j] = atomicSub(s_ptr(ss, tg[j]), 1u);  // :54
+        uint32_t o[2 * U];
+#pragma unroll
+        for (int j = 0; j < 2 * U; j++) {
+            o[j] = kNone;
+            if (tg[j] != kNone) {
+                if (pv[j] == level + 1) {  // :55-57
+                    st_relaxed(stamp_ptr(ss, tg[j]), K + 1);
+                    o[j] = tg[j];
+                } else if (pv[j] <= level) {
+                    atomicAdd(s_ptr(ss, tg[j]), 1u);  // :58-62 repair
+                }
+            }
+        }
+        emit_many(o, ph, next);
+        if (hit_ctr) {
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                const uint32_t hm = __ballot_sync(kFull, eb[q] != kNone);
+                bool dead = false;
+                if (act[q]) {
+                    const uint32_t sa = st_stamp(ld_state(ss, ea[q]));
+                    dead = sa != 0 && sa < K;
+                }
+                const uint32_t dm = __ballot_sync(kFull, dead);
+                if (lane_id() == 0) {
+                    if (hm) atomicAdd(hit_ctr, static_cast<unsigned long long>(__popc(hm)));
+                    if (dm) atomicAdd(hit_ctr + 1, static_cast<unsigned long long>(__popc(dm)));
+                }
+            }
+        }
+    }
     // A STAGED task's probe range [j0, j1): per kStageA-element chunk of N(a), the matching
     // slice of N(b) (it starts where the previous one ended: both lists are sorted) is copied
     // to shared memory with coalesced loads and searched there; a slice longer than kStageB
@@ -164,14 +285,10 @@ struct PeelPolicy {
         const uint32_t* A = g.adj + k.oa;
         const uint32_t* B = g.adj + k.ob;
         const uint32_t nbt = k.lb & ~kStaged, b = k.aux;
-        uint32_t lo = 0;
-        if (lane == 0) lo = lower_bound_u32(B, nbt, A[j0]);
-        lo = __shfl_sync(kFull, lo, 0);
+        uint32_t lo = warp_bound_u32<false>(B, nbt, A[j0]);
         for (uint32_t c0 = j0; c0 < j1; c0 += kStageA) {
             const uint32_t c1 = min(j1, c0 + kStageA);
-            uint32_t hi = 0;
-            if (lane == 0) hi = lo + upper_bound_u32(B + lo, nbt - lo, A[c1 - 1]);
-            hi = __shfl_sync(kFull, hi, 0);
+            const uint32_t hi = lo + warp_bound_u32<true>(B + lo, nbt - lo, A[c1 - 1]);
             const uint32_t nbr = hi - lo;
             if (nbr <= kStageB) {
                 for (uint32_t q = lane; q < nbr; q += 32) stage[q] = B[lo + q];
@@ -453,34 +570,77 @@ __device__ void phase_compact_long(const DevGraph& g, unsigned long long* ss, ui
     }
 }
 
-// Pass 2 (short lists): one warp each, ballot compaction in list order.
+// Pass 2 (short lists): a warp takes a tile of 32 consecutive vertices and walks their
+// live entries as one flat item range (32*kCompactU items per round, lane -> vertex by a
+// shuffle search over the tile's prefix), so short lists fill the lanes and every lane
+// keeps kCompactU state loads in flight. Writes stay in list order: an entry's new slot is
+// its list's kept count before this round (per-vertex counter in shared memory) plus the
+// kept entries before it in the round.
+constexpr int kCompactU = 4;
 __device__ void phase_compact_short(const DevGraph& g, unsigned long long* ss, uint32_t K) {
-    const uint32_t lane = lane_id();
+    __shared__ uint32_t sh_kept[kWarps][32];
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
-    for (uint32_t u = gw; u < g.n; u += nw) {
-        const uint32_t len = g.dl[u];
-        if (len == 0 || len > kBigList) continue;
-        uint32_t* adj = g.adj + g.off[u];
-        uint32_t* eid = g.eid + g.off[u];
-        uint32_t wp = 0;
-        for (uint32_t c = 0; c < len; c += 32) {
-            const uint32_t idx = c + lane;
-            uint32_t a = 0, e = 0;
-            bool keep = false;
-            if (idx < len) {
-                a = adj[idx];
-                e = eid[idx];
-                keep = !processed_stamp(ld_relaxed(stamp_ptr(ss, e)), K);
-            }
-            const uint32_t bal = __ballot_sync(kFull, keep);
-            if (keep) {
-                const uint32_t pos = wp + __popc(bal & lanemask_lt());
-                adj[pos] = a;
-                eid[pos] = e;
-            }
-            wp += __popc(bal);
+    for (uint64_t v0 = uint64_t(gw) * 32; v0 < g.n; v0 += uint64_t(nw) * 32) {
+        const uint64_t u = v0 + lane;
+        uint32_t len = 0, o = 0;
+        if (u < g.n) {
+            len = g.dl[u];
+            if (len > kBigList) len = 0;
         }
-        if (lane == 0) g.dl[u] = wp;
+        const uint32_t incl = warp_incl_scan(len), excl = incl - len;
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        if (total == 0) continue;
+        if (len) o = g.off[u];
+        sh_kept[wid][lane] = 0;
+        __syncwarp();
+        for (uint32_t r0 = 0; r0 < total; r0 += 32u * kCompactU) {
+            uint32_t a[kCompactU], e[kCompactU], st[kCompactU], own[kCompactU], slot[kCompactU];
+#pragma unroll
+            for (int q = 0; q < kCompactU; q++) {
+                const uint32_t item = r0 + 32u * q + lane;
+                own[q] = warp_search_le(excl, item);
+                const uint32_t ob = __shfl_sync(kFull, o, own[q]);
+                const uint32_t ex = __shfl_sync(kFull, excl, own[q]);
+                slot[q] = ob + (item - ex);
+                a[q] = 0;
+                e[q] = 0;
+                if (item < total) {
+                    a[q] = g.adj[slot[q]];
+                    e[q] = g.eid[slot[q]];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kCompactU; q++)
+                st[q] = (r0 + 32u * q + lane < total) ? ld_relaxed(stamp_ptr(ss, e[q])) : 0u;
+            __syncwarp();  // every read of this round precedes every write
+#pragma unroll
+            for (int q = 0; q < kCompactU; q++) {
+                const bool act = r0 + 32u * q + lane < total;
+                const bool keep = act && !processed_stamp(st[q], K);
+                const uint32_t bal = __ballot_sync(kFull, keep);
+                const uint32_t prev_own = __shfl_up_sync(kFull, own[q], 1);
+                const uint32_t heads = __ballot_sync(kFull, lane == 0 || own[q] != prev_own);
+                const uint32_t le = lanemask_lt() | (1u << lane);
+                const uint32_t seg_lo = 31u - __clz(heads & le);
+                const uint32_t segmask = ~((1u << seg_lo) - 1u);
+                const uint32_t before = __popc(bal & lanemask_lt() & segmask);
+                const uint32_t kept0 = sh_kept[wid][own[q]];
+                const uint32_t ob = __shfl_sync(kFull, o, own[q]);
+                if (keep) {
+                    g.adj[ob + kept0 + before] = a[q];
+                    g.eid[ob + kept0 + before] = e[q];
+                }
+                const uint32_t next_own = __shfl_down_sync(kFull, own[q], 1);
+                const bool tail = act && (lane == 31 || next_own != own[q] ||
+                                          r0 + 32u * q + lane + 1 >= total);
+                __syncwarp();
+                if (tail) sh_kept[wid][own[q]] = kept0 + before + (keep ? 1u : 0u);
+                __syncwarp();
+            }
+        }
+        if (len) g.dl[u] = sh_kept[wid][lane];
+        __syncwarp();
     }
 }
 

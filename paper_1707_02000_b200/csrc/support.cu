@@ -48,6 +48,7 @@ struct SupportPolicy {
     uint32_t* ocnt;
     const uint32_t* elems;
     static constexpr bool kHasStaged = false;
+    static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ bool staged(const ITask&) const { return false; }
     __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
@@ -84,6 +85,7 @@ struct CountPolicy {
     const uint32_t* elems;
     unsigned long long count = 0;
     static constexpr bool kHasStaged = false;
+    static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ bool staged(const ITask&) const { return false; }
     __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}

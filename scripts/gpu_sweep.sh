@@ -2,7 +2,7 @@
 IFS=';' read -ra VS <<< "$VARIANTS"
 for v in "${VS[@]}"; do
   name="${v%%:*}"; flags="${v#*:}"
-  make -s -C paper_1707_02000_b200/csrc clean >/dev/null; make -s -C paper_1707_02000_b200/csrc -j16 NVEXTRA="$flags" 2>&1 | grep -E "error"
+  touch paper_1707_02000_b200/csrc/peel.cu; make -s -C paper_1707_02000_b200/csrc -j16 NVEXTRA="$flags" 2>&1 | grep -E "error"
   for c in ${CONFIGS:-3}; do echo "== $name C$c"; TDG_COUNT_HITS=${COUNT:-0} timeout 900 python scripts/run_one.py $c ${REPS:-1} 2>&1 | tail -1 | python -c "
 import sys,ast
 l=sys.stdin.read(); d=ast.literal_eval(l[l.index('{'):])
