@@ -87,6 +87,7 @@ typedef struct tdg_times {
     uint64_t dead_probes; /* probes of already-processed slots (same diagnostic switch)   */
     uint32_t t_max;     /* max trussness (0 when m == 0)                                  */
     uint32_t kernel_launches; /* kernels this call launched                               */
+    double compact_ms;  /*   of process_ms: adjacency compactions (device clock)          */
 } tdg_times;
 
 typedef struct tdg_graph_stats {

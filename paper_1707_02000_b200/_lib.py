@@ -48,7 +48,7 @@ class tdg_times(C.Structure):
                                           "process_ms", "d2h_ms", "total_ms")] + \
                [(k, C.c_uint64) for k in ("triangles", "support_probes", "levels", "sublevels", "scans", "compactions", "probes", "hits",
                                           "dead_probes")] + \
-               [("t_max", C.c_uint32), ("kernel_launches", C.c_uint32)]
+               [("t_max", C.c_uint32), ("kernel_launches", C.c_uint32), ("compact_ms", C.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -84,6 +84,7 @@ struct tdg_context {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx;
+    DevBuf cchunk, cscr, pbits;
     DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab, Ls, bhist, bcur, trace;
     DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing;
     HostCtl* hctl = nullptr;
@@ -132,7 +133,12 @@ struct tdg_context {
         }
         bcur.ensure(kBuckets * 4, "bcur");
         nsl.ensure((n + 2) * 4, "nsl");
+        const uint64_t cc = chunk_cap(m);
+        cchunk.ensure(cc * 12, "compaction chunks");
+        cscr.ensure(m * 16, "compaction scratch");
+        pbits.ensure((m + 31) / 32 * 4, "processed bitmap");
     }
+    static uint64_t chunk_cap(uint64_t m) { return (2 * m) / 512 + (2 * m) / 2048 + 2; }
 
     BuildBufs build_bufs(const int64_t* off64_dev) const {
         BuildBufs b;
@@ -203,13 +209,20 @@ struct tdg_context {
             p.trace = trace.as<unsigned long long>();
             p.trace_cap = static_cast<uint32_t>(trace.cap / 32);
         }
+        const uint64_t cc = cchunk.cap / 12;
+        p.chunk_cap = static_cast<uint32_t>(cc);
+        p.chunks = cchunk.as<uint2>();
+        p.ckept = reinterpret_cast<uint32_t*>(p.chunks + cc);
+        p.sadj = cscr.as<uint32_t>();
+        p.seid = p.sadj ? p.sadj + cscr.cap / 8 : nullptr;
+        p.pbits = pbits.as<uint32_t>();
         return p;
     }
     void trim() {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
                          &osrc, &stask, &sx, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
                          &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &Ls, &bhist, &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1,
-                         &kwpre, &kctl, &ktmp, &knoff, &knadj, &kperm, &kbad, &ing};
+                         &kwpre, &kctl, &ktmp, &knoff, &knadj, &kperm, &kbad, &ing, &cchunk, &cscr, &pbits};
         for (DevBuf* b : all) b->release();
     }
     KcoreBufs kcore_bufs(uint64_t n, uint64_t m) {
@@ -436,6 +449,7 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
             times->compactions = pc.compactions;
             times->scan_ms = pc.scan_ns * 1e-6;
             times->process_ms = pc.proc_ns * 1e-6;
+            times->compact_ms = pc.compact_ns * 1e-6;
             times->probes = pc.probes;
             times->hits = pc.hits;
             times->dead_probes = pc.dead;

@@ -498,6 +498,18 @@ __device__ void phase_prep(const DevGraph& g, const uint32_t* curr, uint32_t cs,
     }, wpre, bsum);
 }
 
+// Processed-edge bitmap (m bits: 65 MB at m = 523M, L2-resident) for the compaction, so
+// that filtering a list costs an L2 lookup per entry instead of a DRAM sector.
+__device__ void mark_processed(uint32_t* pbits, const uint32_t* curr, uint32_t cs) {
+    for (uint32_t t = blockIdx.x * kPeelThreads + threadIdx.x; t < cs; t += gridDim.x * kPeelThreads) {
+        const uint32_t e = curr[t];
+        atomicOr(&pbits[e >> 5], 1u << (e & 31));
+    }
+}
+__device__ __forceinline__ bool processed_bit(const uint32_t* pbits, uint32_t e) {
+    return (ld_relaxed(pbits + (e >> 5)) >> (e & 31)) & 1u;
+}
+
 // process_sublevel (truss_parallel.cpp:39-104) for curr[0..cs) on the intersection engine.
 __device__ unsigned long long phase_process(const DevGraph& g, unsigned long long* ss, uint32_t level,
                                             uint32_t K, const uint32_t* curr, uint32_t cs,
@@ -511,62 +523,90 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
 }
 
 // Adjacency compaction (between levels): drop processed edges (0 < stamp < K) from every
-// live list, in place and order-preserving, and shrink dl. Lists longer than kBigList are
-// compacted by a whole block (block scan per 1024-entry chunk), the rest by one warp
-// (ballot per 32 entries). Processed edges are skipped by every probe anyway (:85), so
-// this only removes work; triangle sets seen by the peel are unchanged.
+// live list, in place and order-preserving, and shrink dl. Lists of original degree above
+// kBigList go through fixed chunks (below), the rest through flat warp tiles. Processed
+// edges are skipped by every probe anyway (:85), so this only removes work; triangle sets
+// seen by the peel are unchanged.
 constexpr uint32_t kBigList = 2048;
 #ifndef TDG_COMPACT_NUM
-#define TDG_COMPACT_NUM 19  // compact once live edges <= NUM/DEN of those at the last compaction
-#define TDG_COMPACT_DEN 20
+#define TDG_COMPACT_NUM 9  // compact once live edges <= NUM/DEN of those at the last compaction
+#define TDG_COMPACT_DEN 10
 #endif
 constexpr unsigned long long kCompactNum = TDG_COMPACT_NUM, kCompactDen = TDG_COMPACT_DEN;
 
-__device__ __forceinline__ bool processed_stamp(uint32_t st, uint32_t K) { return st != 0 && st < K; }
 
-// Pass 1 (long lists). Must be separated from pass 2 by a grid barrier: pass 1 shrinks dl,
-// which would otherwise let pass 2 see a list being compacted as "short".
-__device__ void phase_compact_long(const DevGraph& g, unsigned long long* ss, uint32_t K) {
-    __shared__ uint32_t sh_big[kPeelThreads], sh_nbig;
-    // 1) long lists: one block each (found per 256-vertex tile)
-    for (uint64_t u0 = uint64_t(blockIdx.x) * kPeelThreads; u0 < g.n; u0 += uint64_t(gridDim.x) * kPeelThreads) {
-        if (threadIdx.x == 0) sh_nbig = 0;
-        __syncthreads();
-        const uint64_t uu = u0 + threadIdx.x;
-        if (uu < g.n && g.dl[uu] > kBigList) sh_big[atomicAdd(&sh_nbig, 1u)] = static_cast<uint32_t>(uu);
-        __syncthreads();
-        const uint32_t nbig = sh_nbig;
-        for (uint32_t bi = 0; bi < nbig; bi++) {
-        const uint32_t u = sh_big[bi];
-        const uint32_t len = g.dl[u];
-        uint32_t* adj = g.adj + g.off[u];
-        uint32_t* eid = g.eid + g.off[u];
-        unsigned long long wp = 0;
-        for (uint32_t c = 0; c < len; c += kPeelThreads * 4) {
-            uint32_t a[4], e[4];
-            uint32_t keep = 0, cnt = 0;
+// Long lists (original degree > kBigList) are cut into fixed kChunk-slot chunks
+// {vertex, index} (table built once by k_peel_init), so a hub's list is compacted by many
+// warps at once. Pass A: each warp filters one chunk into the slot-aligned scratch and
+// records its kept count. Pass B (after a grid barrier): each chunk copies its kept
+// entries back to its list at the kept count of the list's earlier chunks; the list's
+// last chunk stores the new live length.
+constexpr uint32_t kChunk = 512;
+constexpr int kCompactU = 4;  // entries per lane per compaction round
+
+__device__ __forceinline__ bool long_list(const DevGraph& g, uint32_t u) { return g.off[u + 1] - g.off[u] > kBigList; }
+
+__device__ void phase_compact_long(const DevGraph& g, unsigned long long* ss, uint32_t K, const PeelBufs& pb,
+                                   uint32_t nchunks) {
+    const uint32_t lane = lane_id();
+    const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
+    for (uint32_t c = gw; c < nchunks; c += nw) {
+        const uint2 ck = pb.chunks[c];
+        const uint32_t lo = ck.y * kChunk, dlu = g.dl[ck.x];
+        uint32_t kept = 0;
+        if (lo < dlu) {
+            const uint32_t hi = min(dlu, lo + kChunk), o = g.off[ck.x];
+            for (uint32_t r0 = lo; r0 < hi; r0 += 32u * kCompactU) {
+                uint32_t a[kCompactU], e[kCompactU], st[kCompactU];
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const uint32_t idx = c + threadIdx.x * 4 + q;  // 4 consecutive: order kept
-                a[q] = 0;
-                e[q] = 0;
-                if (idx < len) {
-                    a[q] = adj[idx];
-                    e[q] = eid[idx];
-                    if (!processed_stamp(ld_relaxed(stamp_ptr(ss, e[q])), K)) { keep |= 1u << q; cnt++; }
+                for (int q = 0; q < kCompactU; q++) {
+                    const uint32_t i = r0 + 32u * q + lane;
+                    a[q] = 0;
+                    e[q] = 0;
+                    if (i < hi) {
+                        a[q] = g.adj[o + i];
+                        e[q] = g.eid[o + i];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < kCompactU; q++)
+                    st[q] = (r0 + 32u * q + lane < hi) ? processed_bit(pb.pbits, e[q]) : 0u;
+#pragma unroll
+                for (int q = 0; q < kCompactU; q++) {
+                    const bool keep = r0 + 32u * q + lane < hi && !st[q];
+                    const uint32_t bal = __ballot_sync(kFull, keep);
+                    if (keep) {
+                        const uint32_t at = o + lo + kept + __popc(bal & lanemask_lt());
+                        pb.sadj[at] = a[q];
+                        pb.seid[at] = e[q];
+                    }
+                    kept += __popc(bal);
                 }
             }
-            unsigned long long tot;
-            unsigned long long pos = wp + block_excl_scan64<kPeelThreads>(cnt, tot);
+        }
+        if (lane == 0) pb.ckept[c] = kept;
+    }
+}
+
+__device__ void phase_compact_copy(const DevGraph& g, const PeelBufs& pb, uint32_t nchunks) {
+    const uint32_t lane = lane_id();
+    const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
+    for (uint32_t c = gw; c < nchunks; c += nw) {
+        const uint2 ck = pb.chunks[c];
+        const uint32_t kept = pb.ckept[c];
+        const uint32_t deg = g.off[ck.x + 1] - g.off[ck.x];
+        const bool last = (ck.y + 1) * kChunk >= deg;
+        if (kept == 0 && !last) continue;
+        uint32_t before = 0;  // kept entries of the list's chunks 0 .. ck.y-1 (at c-ck.y ..)
+        for (uint32_t k = lane; k < ck.y; k += 32) before += pb.ckept[c - ck.y + k];
 #pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (keep & (1u << q)) { adj[pos] = a[q]; eid[pos] = e[q]; pos++; }
-            wp += tot;
-            __syncthreads();
+        for (int d = 16; d > 0; d >>= 1) before += __shfl_xor_sync(kFull, before, d);
+        const uint32_t o = g.off[ck.x], src = o + ck.y * kChunk;
+        for (uint32_t i = lane; i < kept; i += 32) {
+            g.adj[o + before + i] = pb.sadj[src + i];
+            g.eid[o + before + i] = pb.seid[src + i];
         }
-        if (threadIdx.x == 0) g.dl[u] = static_cast<uint32_t>(wp);
-        }
-        __syncthreads();
+        if (last && lane == 0) g.dl[ck.x] = before + kept;
     }
 }
 
@@ -576,18 +616,14 @@ __device__ void phase_compact_long(const DevGraph& g, unsigned long long* ss, ui
 // keeps kCompactU state loads in flight. Writes stay in list order: an entry's new slot is
 // its list's kept count before this round (per-vertex counter in shared memory) plus the
 // kept entries before it in the round.
-constexpr int kCompactU = 4;
-__device__ void phase_compact_short(const DevGraph& g, unsigned long long* ss, uint32_t K) {
+__device__ void phase_compact_short(const DevGraph& g, const uint32_t* pbits) {
     __shared__ uint32_t sh_kept[kWarps][32];
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
     for (uint64_t v0 = uint64_t(gw) * 32; v0 < g.n; v0 += uint64_t(nw) * 32) {
         const uint64_t u = v0 + lane;
         uint32_t len = 0, o = 0;
-        if (u < g.n) {
-            len = g.dl[u];
-            if (len > kBigList) len = 0;
-        }
+        if (u < g.n && !long_list(g, static_cast<uint32_t>(u))) len = g.dl[u];
         const uint32_t incl = warp_incl_scan(len), excl = incl - len;
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         if (total == 0) continue;
@@ -612,12 +648,12 @@ __device__ void phase_compact_short(const DevGraph& g, unsigned long long* ss, u
             }
 #pragma unroll
             for (int q = 0; q < kCompactU; q++)
-                st[q] = (r0 + 32u * q + lane < total) ? ld_relaxed(stamp_ptr(ss, e[q])) : 0u;
+                st[q] = (r0 + 32u * q + lane < total) ? processed_bit(pbits, e[q]) : 0u;
             __syncwarp();  // every read of this round precedes every write
 #pragma unroll
             for (int q = 0; q < kCompactU; q++) {
                 const bool act = r0 + 32u * q + lane < total;
-                const bool keep = act && !processed_stamp(st[q], K);
+                const bool keep = act && !st[q];
                 const uint32_t bal = __ballot_sync(kFull, keep);
                 const uint32_t prev_own = __shfl_up_sync(kFull, own[q], 1);
                 const uint32_t heads = __ballot_sync(kFull, lane == 0 || own[q] != prev_own);
@@ -661,6 +697,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
     bool implicit = true;
     unsigned long long t_prev = leader ? gtimer() : 0;
     unsigned long long sub_w = 0;
+    const uint32_t nchunks = vload(&ctl->nchunks);
     while (true) {
         // ---- scan at `level` (one grid barrier)
         if (leader) { reset_ctr(&ctl->ph[(j + 1) % 3]); ctl->scans++; }
@@ -683,10 +720,12 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         if (level > 0 && (static_cast<unsigned long long>(cs) + nA) * kCompactDen <
                              static_cast<unsigned long long>(live_at_compact) * kCompactNum) {
             if (leader) { reset_ctr(&ctl->ph[(j + 1) % 3]); ctl->compactions++; }
-            phase_compact_long(g, pb.ss, K);
+            phase_compact_long(g, pb.ss, K, pb, nchunks);
+            phase_compact_short(g, pb.pbits);
             grid.sync();
-            phase_compact_short(g, pb.ss, K);
+            phase_compact_copy(g, pb, nchunks);
             grid.sync();
+            if (leader) { const unsigned long long t = gtimer(); ctl->compact_ns += t - t_prev; }
             j++;
             live_at_compact = cs + nA;
         }
@@ -698,6 +737,9 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                 ctl->levels_len = level + 1;
                 reset_ctr(&ctl->ph[(j + 1) % 3]);
             }
+            // curr's edges are processed once this sub-level ends; the bits are read only by
+            // the next compaction (after at least one more grid barrier)
+            mark_processed(pb.pbits, pb.L[li], cs);
             if (level > 0) {  // level 0: s[e1] == 0 bounds its live triangles to none
                 const uint32_t* tasks = pb.L[li];
                 if (kSortMin && cs >= kSortMin) {  // group big sub-levels by searched vertex
@@ -747,9 +789,19 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
 
 __global__ void k_peel_init(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ dl,
                             const uint32_t* __restrict__ s, uint32_t m, unsigned long long* __restrict__ ss,
-                            PeelCtl* ctl) {
-    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x)
-        dl[u] = off[u + 1] - off[u];
+                            PeelCtl* ctl, uint2* chunks, uint32_t chunk_cap) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        const uint32_t deg = off[u + 1] - off[u];
+        dl[u] = deg;
+        if (chunks && deg > kBigList) {  // compaction chunk table (order irrelevant)
+            const uint32_t nc = (deg + kChunk - 1) / kChunk;
+            const uint32_t base = atomicAdd(&ctl->nchunks, nc);
+            if (base + nc <= chunk_cap)
+                for (uint32_t k = 0; k < nc; k++) chunks[base + k] = make_uint2(u, k);
+            else
+                ctl->overflow = 1;
+        }
+    }
     if (ss)  // pack the support pass result with stamp 0
         for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) ss[e] = s[e];
     if (blockIdx.x == 0 && threadIdx.x < 3) reset_ctr(&ctl->ph[threadIdx.x]);
@@ -821,7 +873,8 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     if (err != cudaSuccess) return err;
     if ((err = cudaMemsetAsync(p.nsl, 0, size_t(p.nsl_cap) * sizeof(uint32_t), st)) != cudaSuccess) return err;
     if (g.m == 0) return cudaSuccess;
-    k_peel_init<<<148 * 4, 256, 0, st>>>(g.off, g.n, g.dl, p.s, g.m, p.ss, p.ctl);
+    if (p.pbits && (err = cudaMemsetAsync(p.pbits, 0, size_t((g.m + 31) / 32) * 4, st)) != cudaSuccess) return err;
+    k_peel_init<<<148 * 4, 256, 0, st>>>(g.off, g.n, g.dl, p.s, g.m, p.ss, p.ctl, p.chunks, p.chunk_cap);
     int per_sm = 0;
     err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel, kPeelThreads, 0);
     if (err != cudaSuccess) return err;
@@ -856,7 +909,7 @@ cudaError_t launch_step_process(const DevGraph& g, const PeelBufs& p, uint32_t l
                                 uint8_t* in_curr, uint8_t* in_next, uint8_t* processed, int sm_count,
                                 cudaStream_t st) {
     const uint32_t nchunks = static_cast<uint32_t>(sm_count);
-    k_peel_init<<<sm_count, 256, 0, st>>>(g.off, g.n, g.dl, nullptr, 0, nullptr, p.ctl);
+    k_peel_init<<<sm_count, 256, 0, st>>>(g.off, g.n, g.dl, nullptr, 0, nullptr, p.ctl, nullptr, 0);
     k_step_stamps<<<sm_count * 2, 256, 0, st>>>(processed, in_curr, p.s, g.m, p.ss, p.ctl);
     k_step_prep<<<nchunks, kPeelThreads, 0, st>>>(g, p, curr_size);
     k_step_process<<<sm_count * 2, kPeelThreads, 0, st>>>(g, p, curr_size, level, nchunks);

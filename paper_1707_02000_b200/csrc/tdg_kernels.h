@@ -135,12 +135,13 @@ struct PeelCtl {
     uint32_t overflow;
     uint32_t final_stamp;
     uint32_t t_max;
-    uint32_t pad;
+    uint32_t nchunks;  // long-list compaction chunks (built by k_peel_init)
     unsigned long long scan_ns;  // device-clock time in scan phases (leader thread)
     unsigned long long proc_ns;  // device-clock time in sub-level phases
     unsigned long long probes;   // probe items over all sub-levels (sum of W)
     unsigned long long hits;     // triangle visits (only when PeelBufs::count_hits)
     unsigned long long dead;     // probes whose own slot was already processed (diagnostic)
+    unsigned long long compact_ns;  // device-clock time in adjacency compactions
 };
 struct PeelBufs {
     uint32_t* s;               // support (u32): input of the peel / step-function I/O
@@ -159,6 +160,14 @@ struct PeelBufs {
     uint32_t bshift;      // bucket = vertex >> bshift
     unsigned long long* trace;  // diagnostic (TDG_TRACE): 4 words per sub-level, or null
     uint32_t trace_cap;
+    // compaction of long lists (degree > kBigList): fixed 512-slot chunks {vertex, index},
+    // per-chunk kept counts, and a slot-aligned scratch copy of the kept entries
+    uint2* chunks;
+    uint32_t* ckept;
+    uint32_t chunk_cap;
+    uint32_t* sadj;
+    uint32_t* seid;
+    uint32_t* pbits;  // (m+31)/32 words: bit e set once edge e's sub-level has run
 };
 constexpr uint32_t kBuckets = 1u << 16;
 // Whole level loop in one persistent cooperative launch.
