@@ -157,6 +157,34 @@ __global__ void k_sscatter(const uint32_t* __restrict__ src, const uint32_t* __r
     }
 }
 
+// ---- internal edge ids (truss / support paths): id of edge {x,y} = its ORIENTED SLOT, the
+// position of x->y (x before y in the (degree, id) order) in oadj. Edges of a vertex toward
+// higher-ranked neighbours are then consecutive ids in list order, so the per-triangle state
+// reads and atomics of a probe walk over a list are coalesced instead of random; results are
+// scattered back to reference edge ids (oeid) at the end.
+__global__ void k_r2i(const uint32_t* __restrict__ oeid, uint32_t m, uint32_t* __restrict__ r2i) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) r2i[oeid[t]] = t;
+}
+
+__global__ void k_eid_internal(uint32_t* __restrict__ eid, const uint32_t* __restrict__ r2i, uint64_t slots) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
+         j += uint64_t(gridDim.x) * blockDim.x)
+        eid[j] = r2i[eid[j]];
+}
+
+__global__ void k_el_internal(const uint32_t* __restrict__ osrc, const uint32_t* __restrict__ oadj, uint32_t m,
+                              uint2* __restrict__ el) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x)
+        el[t] = make_uint2(osrc[t], oadj[t]);
+}
+
+// out[oeid[t]] = in[t] + add: an internal-id array back in reference edge-id order.
+__global__ void k_to_ref(const uint32_t* __restrict__ oeid, const uint32_t* __restrict__ in, uint32_t m, uint32_t add,
+                         uint32_t* __restrict__ out) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x)
+        out[oeid[t]] = in[t] + add;
+}
+
 struct MaxOp {
     __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
 };
@@ -244,6 +272,26 @@ cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_o
     if (err != cudaSuccess) return err;
     k_sscatter<<<gs, kThreads, 0, st>>>(b.src, b.flag, b.pos, slots, b.stask, b.sx);
     (*launches) += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_internal_ids(const BuildBufs& b, uint32_t m, uint32_t* r2i, cudaStream_t st, uint32_t* launches) {
+    if (m == 0) return cudaSuccess;
+    const unsigned gm = grid_for(m) > 148u * 32u ? 148u * 32u : grid_for(m);
+    const unsigned gs = grid_for(2ull * m) > 148u * 64u ? 148u * 64u : grid_for(2ull * m);
+    k_r2i<<<gm, kThreads, 0, st>>>(b.oeid, m, r2i);
+    k_eid_internal<<<gs, kThreads, 0, st>>>(b.eid, r2i, 2ull * m);
+    k_el_internal<<<gm, kThreads, 0, st>>>(b.osrc, b.oadj, m, b.el);
+    (*launches) += 3;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_to_ref(const uint32_t* oeid, const uint32_t* in, uint32_t m, uint32_t add, uint32_t* out,
+                          cudaStream_t st, uint32_t* launches) {
+    if (m == 0) return cudaSuccess;
+    const unsigned gm = grid_for(m) > 148u * 32u ? 148u * 32u : grid_for(m);
+    k_to_ref<<<gm, kThreads, 0, st>>>(oeid, in, m, add, out);
+    (*launches)++;
     return cudaGetLastError();
 }
 

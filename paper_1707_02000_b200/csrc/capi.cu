@@ -335,7 +335,10 @@ Dims check_graph(const tdg_csr* g, bool host_ptrs) {
 }
 
 // Upload / alias the CSR and build eo/eid/el (+ orientation). Records ev[0], ev[1], ev[2].
-void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, bool orient, bool tables) {
+// internal=true (truss / support): edge ids become oriented slots before the hash tables are
+// filled (build.cu launch_internal_ids); results go back to reference ids via oeid.
+void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, bool orient, bool tables,
+                     bool internal = false) {
     c->ensure_graph(d.n, d.m);
     const int64_t* off64 = g->offsets;
     ck(cudaEventRecord(c->ev[0], c->stream), "event");
@@ -349,6 +352,9 @@ void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, b
     }
     ck(cudaEventRecord(c->ev[1], c->stream), "event");
     ck(launch_build(c->build_bufs(off64), d.n, d.m, orient, c->stream, &c->launches), "build kernels");
+    if (internal)  // flag (2m+1 u32) is free once the build is done
+        ck(launch_internal_ids(c->build_bufs(off64), d.m, c->flag.as<uint32_t>(), c->stream, &c->launches),
+           "internal edge ids");
     if (tables) {
         // neighbour -> edge-id hash tables; their total size is read back once to size htab
         c->hoff4.ensure((size_t(d.n) + 1) * 4, "hoff4");
@@ -393,17 +399,17 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         c->use();
         const Dims d = check_graph(g, host);
         c->launches = 0;
-        stage_and_build(c, g, d, host, true, true);
+        stage_and_build(c, g, d, host, true, true, true);
         c->ensure_peel(d.n, d.m);
         if (std::getenv("TDG_TRACE")) c->trace.ensure(size_t(32) << 20, "trace");
         const DevGraph dg = c->dev_graph(d.n, d.m);
-        ck(launch_support(dg, c->s.as<uint32_t>(), c->flag.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
+        ck(launch_support(dg, c->s.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
                           c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
         uint32_t* sup_dev = nullptr;
         if (support_out && d.m) {
             if (host) { c->sup.ensure(size_t(d.m) * 4, "support copy"); sup_dev = c->sup.as<uint32_t>(); }
             else sup_dev = support_out;
-            ck(cudaMemcpyAsync(sup_dev, c->s.p, size_t(d.m) * 4, cudaMemcpyDeviceToDevice, c->stream), "support copy");
+            ck(launch_to_ref(dg.oeid, c->s.as<uint32_t>(), d.m, 0, sup_dev, c->stream, &c->launches), "support copy");
         }
         ck(cudaEventRecord(c->ev[3], c->stream), "event");
         const PeelBufs pb = c->peel_bufs(d.n);
@@ -411,7 +417,7 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         ck(cudaEventRecord(c->ev[6], c->stream), "event");
         uint32_t* tdev = truss_out;
         if (host) { c->truss.ensure(size_t(d.m) * 4, "truss"); tdev = c->truss.as<uint32_t>(); }
-        ck(launch_finalize(pb.ss, d.m, tdev, pb.ctl, c->stream, &c->launches), "finalize kernel");
+        ck(launch_finalize(pb.ss, dg.oeid, d.m, tdev, pb.ctl, c->stream, &c->launches), "finalize kernel");
         ck(cudaEventRecord(c->ev[4], c->stream), "event");
         if (host && d.m) {
             ck(cudaMemcpyAsync(truss_out, tdev, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H truss");
@@ -465,11 +471,13 @@ int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_
         c->use();
         const Dims d = check_graph(g, host);
         c->launches = 0;
-        stage_and_build(c, g, d, host, true, true);
+        stage_and_build(c, g, d, host, true, false, true);
         const DevGraph dg = c->dev_graph(d.n, d.m);
-        uint32_t* sdev = host ? c->s.as<uint32_t>() : support_out;
-        ck(launch_support(dg, sdev, c->flag.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
+        uint32_t* sdev = support_out;
+        if (host) { c->sup.ensure(size_t(d.m) * 4 + 4, "support copy"); sdev = c->sup.as<uint32_t>(); }
+        ck(launch_support(dg, c->s.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
                           c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
+        ck(launch_to_ref(dg.oeid, c->s.as<uint32_t>(), d.m, 0, sdev, c->stream, &c->launches), "support to ref ids");
         ck(cudaEventRecord(c->ev[3], c->stream), "event");
         if (host && d.m)
             ck(cudaMemcpyAsync(support_out, sdev, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H support");

@@ -807,12 +807,13 @@ __global__ void k_peel_init(const uint32_t* __restrict__ off, uint32_t n, uint32
     if (blockIdx.x == 0 && threadIdx.x < 3) reset_ctr(&ctl->ph[threadIdx.x]);
 }
 
-__global__ void k_finalize(const unsigned long long* __restrict__ ss, uint32_t m, uint32_t* __restrict__ truss,
-                           PeelCtl* ctl) {
+// truss[ref id] = s + 2; ss is indexed by internal id, oeid maps it to the reference edge id.
+__global__ void k_finalize(const unsigned long long* __restrict__ ss, const uint32_t* __restrict__ oeid, uint32_t m,
+                           uint32_t* __restrict__ truss, PeelCtl* ctl) {
     uint32_t mx = 0;
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
         const uint32_t t = static_cast<uint32_t>(ss[e]) + 2;  // truss_parallel.cpp:146-148
-        truss[e] = t;
+        truss[oeid[e]] = t;
         mx = t > mx ? t : mx;
     }
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
@@ -889,10 +890,10 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     return err;
 }
 
-cudaError_t launch_finalize(const unsigned long long* ss, uint32_t m, uint32_t* truss, PeelCtl* ctl, cudaStream_t st,
-                            uint32_t* launches) {
+cudaError_t launch_finalize(const unsigned long long* ss, const uint32_t* oeid, uint32_t m, uint32_t* truss, PeelCtl* ctl,
+                            cudaStream_t st, uint32_t* launches) {
     if (m == 0) return cudaSuccess;
-    k_finalize<<<148 * 4, 256, 0, st>>>(ss, m, truss, ctl);
+    k_finalize<<<148 * 4, 256, 0, st>>>(ss, oeid, m, truss, ctl);
     (*launches)++;
     return cudaGetLastError();
 }

@@ -37,15 +37,14 @@ __device__ __forceinline__ ITask otask(const DevGraph& g, uint32_t t) {
     return k;
 }
 
-// Counts go to ocnt[], indexed by ORIENTED SLOT (position in the N+ arrays), not by edge
-// id: the owner-side slots of a task group are one contiguous, L2-resident N+(x) range and
-// the probe-side slots of one task are consecutive, so the per-triangle atomics stay out of
-// DRAM (edge-id-indexed atomics were random 2 GB read-modify-writes at C5). The task's own
-// edge is counted into s[] directly; k_support_combine adds ocnt[t] into s[oeid[t]].
+// Edge ids are internal (build.cu launch_internal_ids): an edge's id IS its oriented slot
+// (position in the N+ arrays). The owner-side slots of a task group are one contiguous,
+// L2-resident N+(x) range and the probe-side slots of one task are consecutive, so the
+// per-triangle atomics stay out of DRAM (reference-id-indexed atomics were random 2 GB
+// read-modify-writes at C5).
 struct SupportPolicy {
     const DevGraph& g;
     uint32_t* s;
-    uint32_t* ocnt;
     const uint32_t* elems;
     static constexpr bool kHasStaged = false;
     static constexpr int kUnroll = 1;
@@ -60,8 +59,8 @@ struct SupportPolicy {
     // each, the task's edge one per group of lanes sharing it (__match_any_sync).
     __device__ void visit(bool, bool hit, const ITask& k, uint32_t ja, uint32_t p) const {
         if (hit) {
-            atomicAdd(&ocnt[k.oa + ja], 1u);
-            atomicAdd(&ocnt[k.ob + p], 1u);
+            atomicAdd(&s[k.oa + ja], 1u);
+            atomicAdd(&s[k.ob + p], 1u);
         }
         const uint32_t fm = __ballot_sync(kFull, hit);
         if (fm && hit) {
@@ -108,22 +107,13 @@ __global__ void __launch_bounds__(kThreads) k_triangle_count(DevGraph g, const u
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->probes = W;
 }
 
-__global__ void __launch_bounds__(kThreads) k_support(DevGraph g, uint32_t* __restrict__ s, uint32_t* __restrict__ ocnt,
+__global__ void __launch_bounds__(kThreads) k_support(DevGraph g, uint32_t* __restrict__ s,
                                                       const unsigned long long* wpre, const unsigned long long* bsum,
                                                       uint32_t nchunks, SupportCtl* ctl) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
-    SupportPolicy P{g, s, ocnt, g.oadj};
+    SupportPolicy P{g, s, g.oadj};
     const unsigned long long W = process_items<kThreads>(P, g.m, wpre, bsum, nchunks, &ctl->piece_head, sboff);
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->probes = W;
-}
-
-// s[oeid[t]] += ocnt[t] (each edge has exactly one oriented slot), then sum / max.
-__global__ void k_support_combine(const uint32_t* __restrict__ oeid, const uint32_t* __restrict__ ocnt, uint32_t m,
-                                  uint32_t* __restrict__ s) {
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < m; t += gridDim.x * blockDim.x) {
-        const uint32_t c = ocnt[t];
-        if (c) s[oeid[t]] += c;
-    }
 }
 
 __global__ void k_support_sum(const uint32_t* __restrict__ s, uint32_t m, SupportCtl* ctl) {
@@ -146,24 +136,22 @@ __global__ void k_support_sum(const uint32_t* __restrict__ s, uint32_t m, Suppor
 
 }  // namespace
 
-cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint32_t* ocnt, unsigned long long* wpre,
+cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* wpre,
                            unsigned long long* bsum, SupportCtl* ctl, int sm_count, cudaStream_t st,
                            uint32_t* launches) {
     cudaError_t err = cudaMemsetAsync(ctl, 0, sizeof(SupportCtl), st);
     if (err != cudaSuccess) return err;
     if (g.m == 0) return cudaSuccess;
     if ((err = cudaMemsetAsync(s, 0, size_t(g.m) * sizeof(uint32_t), st)) != cudaSuccess) return err;
-    if ((err = cudaMemsetAsync(ocnt, 0, size_t(g.m) * sizeof(uint32_t), st)) != cudaSuccess) return err;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_support, kThreads, 0);
     if (per_sm < 1) per_sm = 1;
     unsigned grid = static_cast<unsigned>(sm_count * per_sm);
     const unsigned nchunks = grid < kMaxChunks ? grid : kMaxChunks;
     k_support_prep<<<nchunks, kThreads, 0, st>>>(g, wpre, bsum);
-    k_support<<<grid, kThreads, 0, st>>>(g, s, ocnt, wpre, bsum, nchunks, ctl);
-    k_support_combine<<<grid, kThreads, 0, st>>>(g.oeid, ocnt, g.m, s);
+    k_support<<<grid, kThreads, 0, st>>>(g, s, wpre, bsum, nchunks, ctl);
     k_support_sum<<<grid, kThreads, 0, st>>>(s, g.m, ctl);
-    (*launches) += 4;
+    (*launches) += 3;
     return cudaGetLastError();
 }
 

@@ -36,6 +36,13 @@ size_t build_cub_bytes(uint32_t n, uint32_t m);
 cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_orientation,
                          cudaStream_t st, uint32_t* launches);
 
+// Internal edge ids (truss / support): after launch_build with orientation, rewrite eid[2m]
+// and el[m] so edge {x,y} is identified by its oriented slot (position in oadj); r2i: m u32
+// scratch. launch_to_ref scatters an internal-id array back: out[oeid[t]] = in[t] + add.
+cudaError_t launch_internal_ids(const BuildBufs& b, uint32_t m, uint32_t* r2i, cudaStream_t st, uint32_t* launches);
+cudaError_t launch_to_ref(const uint32_t* oeid, const uint32_t* in, uint32_t m, uint32_t add, uint32_t* out,
+                          cudaStream_t st, uint32_t* launches);
+
 // Per-vertex neighbour -> edge-id hash tables (tdg_common.cuh). hq: n+1 scratch; the host
 // reads hoff4[n] (total slots / 4) between the two calls to size htab.
 cudaError_t launch_htab_sizes(const uint32_t* off, uint32_t n, uint32_t* hq, uint32_t* hoff4, void* cub_tmp,
@@ -57,8 +64,9 @@ struct SupportCtl {
     unsigned long long probes;  // probe items of the support pass
 };
 constexpr uint32_t kMaxChunks = 1024;  // max blocks of a prep grid (one work chunk each)
-// ocnt: m u32 scratch (per oriented slot); wpre: >= m u64 scratch; bsum: kMaxChunks u64.
-cudaError_t launch_support(const DevGraph& g, uint32_t* s, uint32_t* ocnt, unsigned long long* wpre,
+// Requires internal edge ids (launch_internal_ids): s[m] is indexed by oriented slot.
+// wpre: >= m u64 scratch; bsum: kMaxChunks u64.
+cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* wpre,
                            unsigned long long* bsum, SupportCtl* ctl, int sm_count, cudaStream_t st,
                            uint32_t* launches);
 
@@ -174,7 +182,7 @@ constexpr uint32_t kBuckets = 1u << 16;
 cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cudaStream_t st,
                         uint32_t* launches);
 // truss[e] = s[e] + 2 and t_max.
-cudaError_t launch_finalize(const unsigned long long* ss, uint32_t m, uint32_t* truss, PeelCtl* ctl,
+cudaError_t launch_finalize(const unsigned long long* ss, const uint32_t* oeid, uint32_t m, uint32_t* truss, PeelCtl* ctl,
                             cudaStream_t st, uint32_t* launches);
 
 // Step functions (tdg_scan / tdg_process_sublevel) on reference-style flags.

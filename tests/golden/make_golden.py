@@ -14,6 +14,12 @@ are committed so the GPU box (which has no /root/reference) can check against th
 
 Usage: python tests/golden/make_golden.py fixtures
        python tests/golden/make_golden.py configs 1 2 3 4 [5]   (C3 ~5 min, C5 hours)
+       python tests/golden/make_golden.py configs-kcore 5
+           same record, but the reference runs on its own preprocessed graph
+           (kcore_parallel -> coreness_order -> reorder, trussdec.cpp:92-97) and the
+           per-edge truss / support are mapped back to the input's edge ids by (u,v).
+           Trussness, support and nsl are invariant under vertex relabelling, so the
+           record is the same; the reordered graph peels far faster on a CPU.
 """
 from __future__ import annotations
 
@@ -107,7 +113,48 @@ def fixtures():
     print(f"fixtures.json: {len(out)} graphs")
 
 
-def configs(ids):
+def edge_keys(off, nb) -> np.ndarray:
+    """u<<32|v for every edge u<v in reference edge-id order (graph.cpp:86-99: ascending (u,v))."""
+    n = len(off) - 1
+    deg = np.diff(off)
+    src = np.repeat(np.arange(n, dtype=np.uint32), deg)
+    keep = nb.view(np.uint32) > src
+    k = src[keep].astype(np.uint64) << np.uint64(32)
+    del src
+    k |= nb[keep].astype(np.uint64)
+    return k
+
+
+def mapped_back(R: Reference, g: Csr, workers: int):
+    """Reference pipeline on the reordered graph; truss/support returned in g's edge-id order."""
+    t0 = time.time()
+    core, cmax, perm = R.kcore_order(g, workers)
+    r = R.reorder(g, perm)
+    t1 = time.time()
+    print(f"  kcore+reorder {t1 - t0:.1f}s c_max={cmax}", flush=True)
+    d = R.truss_parallel(r, workers)
+    t2 = time.time()
+    print(f"  truss_parallel {t2 - t1:.1f}s {d.times}", flush=True)
+    sup_r = R.support_am4(r, workers)
+    kr = edge_keys(r.offsets, r.neighbors)
+    del r
+    ko = edge_keys(g.offsets, g.neighbors)
+    p = perm.astype(np.uint64)
+    a = p[(ko >> np.uint64(32)).astype(np.int64)]
+    b = p[(ko & np.uint64(0xFFFFFFFF)).astype(np.int64)]
+    del ko
+    key = (np.minimum(a, b) << np.uint64(32)) | np.maximum(a, b)
+    del a, b
+    idx = np.searchsorted(kr, key)
+    assert (kr[idx] == key).all()
+    del kr, key
+    truss = d.truss[idx]
+    sup = sup_r[idx]
+    d.times["kcore_reorder"] = t1 - t0
+    return d, truss, sup
+
+
+def configs(ids, kcore=False):
     from paper_1707_02000_b200 import graphgen
     R = Reference()
     path = os.path.join(HERE, "configs.json")
@@ -118,8 +165,12 @@ def configs(ids):
         g = Csr(n, m, off, nb)
         tg = time.time() - t0
         workers = int(os.environ.get("TDG_GOLDEN_WORKERS", os.cpu_count() or 8))
-        d = R.truss_parallel(g, workers)
-        sup = R.support_am4(g, workers)
+        if kcore:
+            d, truss, sup = mapped_back(R, g, workers)
+            d.truss = truss
+        else:
+            d = R.truss_parallel(g, workers)
+            sup = R.support_am4(g, workers)
         vals, cnt = np.unique(d.truss, return_counts=True)
         doc["configs"][str(c)] = {
             "name": graphgen.CONFIG_NAMES[c], "n": n, "m": m,
@@ -130,6 +181,7 @@ def configs(ids):
             "triangles": int(sup.astype(np.uint64).sum() // 3),
             "sum_tau_minus_1": int(d.truss.astype(np.uint64).sum() - m),
             "ref_times_s": d.times, "ref_workers": workers, "gen_s": tg,
+            "ref_pipeline": "kcore->coreness_order->reorder, mapped back" if kcore else "input order",
         }
         json.dump(doc, open(path, "w"), indent=1)
         print(f"C{c}: n={n} m={m} t_max={int(d.truss.max())} sublevels={sum(d.nsl)} ({time.time()-t0:.1f}s)")
@@ -139,4 +191,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "fixtures":
         fixtures()
     else:
-        configs([int(x) for x in sys.argv[2:]])
+        configs([int(x) for x in sys.argv[2:]], kcore=sys.argv[1] == "configs-kcore")
