@@ -271,7 +271,8 @@ cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_o
     err = cub::DeviceScan::ExclusiveSum(b.cub_tmp, tmp, b.flag, b.pos, slots + 1, st);
     if (err != cudaSuccess) return err;
     k_sscatter<<<gs, kThreads, 0, st>>>(b.src, b.flag, b.pos, slots, b.stask, b.sx);
-    (*launches) += 2;
+    k_opos<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(b.off, b.pos, n, b.sbeg);  // first task of each owner
+    (*launches) += 3;
     return cudaGetLastError();
 }
 

@@ -83,7 +83,7 @@ struct tdg_context {
     int sms = 148;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
-    DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx;
+    DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx, sbeg;
     DevBuf cchunk, cscr, pbits;
     DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab, Ls, bhist, bcur, trace;
     DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing;
@@ -112,6 +112,7 @@ struct tdg_context {
         osrc.ensure(m * 4, "osrc");
         stask.ensure(m * 4, "stask");
         sx.ensure(m * 4, "sx");
+        sbeg.ensure((n + 1) * 4, "sbeg");
         dl.ensure(n * 4, "dl");
         s.ensure(m * 4, "support");
         ctl.ensure(sizeof(PeelCtl), "ctl");
@@ -159,6 +160,7 @@ struct tdg_context {
         b.osrc = osrc.as<uint32_t>();
         b.stask = stask.as<uint32_t>();
         b.sx = sx.as<uint32_t>();
+        b.sbeg = sbeg.as<uint32_t>();
         b.cub_tmp = cub.p;
         b.cub_bytes = cub.cap;
         return b;
@@ -178,6 +180,7 @@ struct tdg_context {
         g.osrc = osrc.as<uint32_t>();
         g.stask = stask.as<uint32_t>();
         g.sx = sx.as<uint32_t>();
+        g.sbeg = sbeg.as<uint32_t>();
         g.hoff4 = hoff4.as<uint32_t>();
         g.htab = htab.as<unsigned long long>();
         return g;
@@ -220,7 +223,7 @@ struct tdg_context {
     }
     void trim() {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
-                         &osrc, &stask, &sx, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
+                         &osrc, &stask, &sx, &sbeg, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
                          &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &Ls, &bhist, &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1,
                          &kwpre, &kctl, &ktmp, &knoff, &knadj, &kperm, &kbad, &ing, &cchunk, &cscr, &pbits};
         for (DevBuf* b : all) b->release();

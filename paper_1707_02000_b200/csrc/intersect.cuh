@@ -100,6 +100,144 @@ __device__ void prep_items(uint32_t ntasks, WorkF&& work, unsigned long long* wp
     if (threadIdx.x == 0) bsum[blockIdx.x] = run;
 }
 
+// Largest task t with start(t) <= x (start = sboff[t / CH] + wpre[t]).
+__device__ __forceinline__ uint32_t task_at(unsigned long long x, uint32_t ntasks, const unsigned long long* wpre,
+                                            const unsigned long long* sboff, uint32_t nchunks, uint32_t CH) {
+    uint32_t clo = 0, chi = nchunks;
+    while (chi - clo > 1) {
+        const uint32_t mid = (clo + chi) >> 1;
+        if (sboff[mid] <= x) clo = mid; else chi = mid;
+    }
+    uint32_t ilo = clo * CH, ihi = min(ntasks, (clo + 1) * CH);
+    const unsigned long long rel = x - sboff[clo];
+    while (ihi - ilo > 1) {
+        const uint32_t mid = (ilo + ihi) >> 1;
+        if (wpre[mid] <= rel) ilo = mid; else ihi = mid;
+    }
+    return ilo;
+}
+
+// One warp processes work items [x0, x1) of the global axis, starting at the task i that
+// contains x0 (see the file comment).
+template <class Policy>
+__device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsigned long long x1, uint32_t i0,
+                                          uint32_t ntasks, const unsigned long long* wpre,
+                                          const unsigned long long* sboff, uint32_t CH) {
+    const uint32_t lane = lane_id();
+    uint32_t i = i0;
+    // lanes hold tasks i..i+31 (start st); end_held = start of task i+32
+    uint32_t held = kNone;
+    ITask k{0, 0, 0, 0, 0, kNone};
+    unsigned long long st = ~0ull, end_held = ~0ull;
+    for (unsigned long long base = x0; base < x1;) {
+        if (held != i) {
+            // Slide the held window: tasks already held move down by `adv` lanes with
+            // shuffles; only the lanes past the old window load (each task descriptor
+            // costs ~6 random loads, so reloading all 32 per step dominated traffic).
+            const uint32_t adv = (held != kNone && i > held) ? i - held : 32u;
+            if (adv < 32) {
+                k.id = __shfl_down_sync(kFull, k.id, adv);
+                k.oa = __shfl_down_sync(kFull, k.oa, adv);
+                k.la = __shfl_down_sync(kFull, k.la, adv);
+                k.ob = __shfl_down_sync(kFull, k.ob, adv);
+                k.lb = __shfl_down_sync(kFull, k.lb, adv);
+                k.aux = __shfl_down_sync(kFull, k.aux, adv);
+                const uint32_t lo = __shfl_down_sync(kFull, static_cast<uint32_t>(st), adv);
+                const uint32_t hi = __shfl_down_sync(kFull, static_cast<uint32_t>(st >> 32), adv);
+                st = (static_cast<unsigned long long>(hi) << 32) | lo;
+            }
+            const uint32_t t = i + lane;
+            if (lane + adv >= 32) {
+                if (t < ntasks) {
+                    k = P.load(t);
+                    st = sboff[t / CH] + wpre[t];
+                } else {
+                    st = ~0ull;
+                }
+            }
+            unsigned long long s32 = ~0ull;
+            if (lane == 31 && t + 1 < ntasks) s32 = sboff[(t + 1) / CH] + wpre[t + 1];
+            end_held = shfl64(s32, 31);
+            held = i;
+        }
+        unsigned long long limit = x1 < end_held ? x1 : end_held;
+        if (Policy::kHasStaged) {
+            // STAGED tasks (long, comparable lists) run alone over their in-piece range;
+            // the window below stops at the first staged task it holds.
+            const uint32_t smask = __ballot_sync(kFull, P.staged(k));
+            if (smask & 1u) {
+                const unsigned long long st0 = shfl64(st, 0), st1 = shfl64(st, 1);
+                const unsigned long long end0 = st1 < end_held ? st1 : end_held;
+                const unsigned long long lim0 = x1 < end0 ? x1 : end0;
+                P.staged_range(shfl_task(k, 0), static_cast<uint32_t>(base - st0),
+                               static_cast<uint32_t>(lim0 - st0));
+                if (lim0 == end0) i += 1;
+                base = lim0;
+                continue;
+            }
+            if (smask) {
+                const unsigned long long sm = shfl64(st, __ffs(smask) - 1);
+                limit = sm < limit ? sm : limit;
+            }
+        }
+        const uint32_t relk = st <= base ? 0u
+                              : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
+        constexpr int U = Policy::kUnroll;
+        if constexpr (U > 1) {
+            // U items per lane per step (item base + lane + 32q): the policy issues their
+            // independent loads together, so each lane keeps U probe chains in flight.
+            ITask ko[U];
+            uint32_t ja[U];
+            bool act[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                const uint32_t key = lane + 32u * q;
+                const uint32_t own = warp_search_le(relk, key);
+                const unsigned long long so = shfl64(st, own);
+                ko[q] = shfl_task(k, own);
+                const unsigned long long x = base + key;
+                act[q] = x < limit;
+                ja[q] = act[q] ? static_cast<uint32_t>(x - so) : 0u;
+            }
+            P.template run<U>(act, ko, ja);
+        } else {
+            const uint32_t own = warp_search_le(relk, lane);
+            const unsigned long long so = shfl64(st, own);
+            const ITask ko = shfl_task(k, own);
+            const unsigned long long x = base + lane;
+            uint32_t ja = 0, e = kNone;
+            const bool active = x < limit;
+            if (active) {
+                ja = static_cast<uint32_t>(x - so);
+                e = P.find(ko, P.elems[ko.oa + ja]);
+            }
+            P.visit(active, e != kNone, ko, ja, e);
+        }
+        const unsigned long long nb = base + 32u * U < limit ? base + 32u * U : limit;
+        i = (nb >= end_held) ? i + 32 : i + warp_search_le(relk, static_cast<uint32_t>(nb - base));
+        base = nb;
+    }
+}
+
+// sboff[c] = exclusive prefix of the chunk totals bsum[0..nchunks) (block-wide; smem
+// sboff holds >= nchunks+1 entries); returns the total work.
+template <int kThreads>
+__device__ unsigned long long chunk_offsets(const unsigned long long* bsum, uint32_t nchunks, unsigned long long* sboff) {
+    const uint32_t per = (nchunks + kThreads - 1) / kThreads;
+    const uint32_t c0 = threadIdx.x * per;
+    unsigned long long loc = 0;
+    for (uint32_t c = c0; c < c0 + per && c < nchunks; c++) loc += bsum[c];
+    unsigned long long tot;
+    unsigned long long run = block_excl_scan64<kThreads>(loc, tot);
+    for (uint32_t c = c0; c < c0 + per && c < nchunks; c++) {
+        sboff[c] = run;
+        run += bsum[c];
+    }
+    if (threadIdx.x == 0) sboff[nchunks] = tot;
+    __syncthreads();
+    return sboff[nchunks];
+}
+
 // Process all work of tasks [0, ntasks) (see file comment). `piece_head` must be 0 on
 // entry; bsum/wpre come from prep_items over a `nchunks`-block grid. smem: sboff holds
 // >= nchunks+1 entries. Returns the total work W.
@@ -107,20 +245,7 @@ template <int kThreads, class Policy>
 __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const unsigned long long* wpre,
                               const unsigned long long* bsum, uint32_t nchunks, uint32_t* piece_head,
                               unsigned long long* sboff) {
-    {
-        const uint32_t per = (nchunks + kThreads - 1) / kThreads;
-        const uint32_t c0 = threadIdx.x * per;
-        unsigned long long loc = 0;
-        for (uint32_t c = c0; c < c0 + per && c < nchunks; c++) loc += bsum[c];
-        unsigned long long tot;
-        unsigned long long run = block_excl_scan64<kThreads>(loc, tot);
-        for (uint32_t c = c0; c < c0 + per && c < nchunks; c++) {
-            sboff[c] = run;
-            run += bsum[c];
-        }
-        if (threadIdx.x == 0) sboff[nchunks] = tot;
-        __syncthreads();
-    }
+    chunk_offsets<kThreads>(bsum, nchunks, sboff);
     const unsigned long long W = sboff[nchunks];
     if (W == 0) return 0;
     const uint32_t CH = chunk_len(ntasks, nchunks);
@@ -138,111 +263,7 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
         if (p >= npieces) break;
         const unsigned long long x0 = p * PS;
         const unsigned long long x1 = x0 + PS < W ? x0 + PS : W;
-        // task containing x0: largest chunk c with sboff[c] <= x0, then largest t in it
-        uint32_t clo = 0, chi = nchunks;
-        while (chi - clo > 1) {
-            const uint32_t mid = (clo + chi) >> 1;
-            if (sboff[mid] <= x0) clo = mid; else chi = mid;
-        }
-        uint32_t ilo = clo * CH, ihi = min(ntasks, (clo + 1) * CH);
-        const unsigned long long rel = x0 - sboff[clo];
-        while (ihi - ilo > 1) {
-            const uint32_t mid = (ilo + ihi) >> 1;
-            if (wpre[mid] <= rel) ilo = mid; else ihi = mid;
-        }
-        uint32_t i = ilo;
-        // lanes hold tasks i..i+31 (start st); end_held = start of task i+32
-        uint32_t held = kNone;
-        ITask k{0, 0, 0, 0, 0, kNone};
-        unsigned long long st = ~0ull, end_held = ~0ull;
-        for (unsigned long long base = x0; base < x1;) {
-            if (held != i) {
-                // Slide the held window: tasks already held move down by `adv` lanes with
-                // shuffles; only the lanes past the old window load (each task descriptor
-                // costs ~6 random loads, so reloading all 32 per step dominated traffic).
-                const uint32_t adv = (held != kNone && i > held) ? i - held : 32u;
-                if (adv < 32) {
-                    k.id = __shfl_down_sync(kFull, k.id, adv);
-                    k.oa = __shfl_down_sync(kFull, k.oa, adv);
-                    k.la = __shfl_down_sync(kFull, k.la, adv);
-                    k.ob = __shfl_down_sync(kFull, k.ob, adv);
-                    k.lb = __shfl_down_sync(kFull, k.lb, adv);
-                    k.aux = __shfl_down_sync(kFull, k.aux, adv);
-                    const uint32_t lo = __shfl_down_sync(kFull, static_cast<uint32_t>(st), adv);
-                    const uint32_t hi = __shfl_down_sync(kFull, static_cast<uint32_t>(st >> 32), adv);
-                    st = (static_cast<unsigned long long>(hi) << 32) | lo;
-                }
-                const uint32_t t = i + lane;
-                if (lane + adv >= 32) {
-                    if (t < ntasks) {
-                        k = P.load(t);
-                        st = sboff[t / CH] + wpre[t];
-                    } else {
-                        st = ~0ull;
-                    }
-                }
-                unsigned long long s32 = ~0ull;
-                if (lane == 31 && t + 1 < ntasks) s32 = sboff[(t + 1) / CH] + wpre[t + 1];
-                end_held = shfl64(s32, 31);
-                held = i;
-            }
-            unsigned long long limit = x1 < end_held ? x1 : end_held;
-            if (Policy::kHasStaged) {
-                // STAGED tasks (long, comparable lists) run alone over their in-piece range;
-                // the window below stops at the first staged task it holds.
-                const uint32_t smask = __ballot_sync(kFull, P.staged(k));
-                if (smask & 1u) {
-                    const unsigned long long st0 = shfl64(st, 0), st1 = shfl64(st, 1);
-                    const unsigned long long end0 = st1 < end_held ? st1 : end_held;
-                    const unsigned long long lim0 = x1 < end0 ? x1 : end0;
-                    P.staged_range(shfl_task(k, 0), static_cast<uint32_t>(base - st0),
-                                   static_cast<uint32_t>(lim0 - st0));
-                    if (lim0 == end0) i += 1;
-                    base = lim0;
-                    continue;
-                }
-                if (smask) {
-                    const unsigned long long sm = shfl64(st, __ffs(smask) - 1);
-                    limit = sm < limit ? sm : limit;
-                }
-            }
-            const uint32_t relk = st <= base ? 0u
-                                  : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
-            constexpr int U = Policy::kUnroll;
-            if constexpr (U > 1) {
-                // U items per lane per step (item base + lane + 32q): the policy issues their
-                // independent loads together, so each lane keeps U probe chains in flight.
-                ITask ko[U];
-                uint32_t ja[U];
-                bool act[U];
-#pragma unroll
-                for (int q = 0; q < U; q++) {
-                    const uint32_t key = lane + 32u * q;
-                    const uint32_t own = warp_search_le(relk, key);
-                    const unsigned long long so = shfl64(st, own);
-                    ko[q] = shfl_task(k, own);
-                    const unsigned long long x = base + key;
-                    act[q] = x < limit;
-                    ja[q] = act[q] ? static_cast<uint32_t>(x - so) : 0u;
-                }
-                P.template run<U>(act, ko, ja);
-            } else {
-                const uint32_t own = warp_search_le(relk, lane);
-                const unsigned long long so = shfl64(st, own);
-                const ITask ko = shfl_task(k, own);
-                const unsigned long long x = base + lane;
-                uint32_t ja = 0, e = kNone;
-                const bool active = x < limit;
-                if (active) {
-                    ja = static_cast<uint32_t>(x - so);
-                    e = P.find(ko, P.elems[ko.oa + ja]);
-                }
-                P.visit(active, e != kNone, ko, ja, e);
-            }
-            const unsigned long long nb = base + 32u * U < limit ? base + 32u * U : limit;
-            i = (nb >= end_held) ? i + 32 : i + warp_search_le(relk, static_cast<uint32_t>(nb - base));
-            base = nb;
-        }
+        run_items(P, x0, x1, task_at(x0, ntasks, wpre, sboff, nchunks, CH), ntasks, wpre, sboff, CH);
     }
     return W;
 }

@@ -13,6 +13,8 @@
 // the warp with __match_any_sync and one atomicAdd per group; the other two edges get one
 // atomicAdd each. No X[n] scratch.
 
+#include <cstdlib>
+
 #include "intersect.cuh"
 #include "tdg_kernels.h"
 
@@ -69,6 +71,127 @@ struct SupportPolicy {
         }
     }
 };
+
+// ---- owner-table form. A block takes a piece of the work axis and walks its owner
+// segments (the tasks of one owner x are contiguous, [sbeg[x], sbeg[x+1])). For a segment
+// with enough work, N+(x) is loaded once into a shared-memory hash table (key c -> its
+// position in N+(x)) and the block's 8 warps split the segment's items evenly; each probe is then
+// one coalesced N+(y) load plus ~1 shared-memory access instead of a log2(d+(x)) chain of
+// L1 loads (the search form is issue-bound: ncu C3, 71% issue slots busy). Segments that
+// are too small to pay for the table, or whose owner list exceeds the table, are batched
+// and searched in global memory as before.
+#ifndef TDG_SUP_TAB
+#define TDG_SUP_TAB 4096  // shared-memory table slots (8 B each): owners with d+ <= TAB/2
+#endif
+constexpr uint32_t kSupTab = TDG_SUP_TAB;
+constexpr uint32_t kSupWarps = kThreads / 32;
+
+struct SupportTabPolicy {
+    const DevGraph& g;
+    uint32_t* s;
+    const uint32_t* elems;
+    const uint2* tab;
+    uint32_t mask;
+    static constexpr bool kHasStaged = false;
+    static constexpr int kUnroll = 1;
+    __device__ ITask load(uint32_t t) const { return otask(g, t); }
+    __device__ bool staged(const ITask&) const { return false; }
+    __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
+    __device__ uint32_t find(const ITask&, uint32_t c) const {
+        uint32_t h = hmix(c) & mask;
+        while (true) {
+            const uint2 e = tab[h];
+            if (e.x == c) return e.y;
+            if (e.x == kHEmpty) return kNone;
+            h = (h + 1) & mask;
+        }
+    }
+    __device__ void visit(bool a, bool hit, const ITask& k, uint32_t ja, uint32_t p) const {
+        SupportPolicy{g, s, elems}.visit(a, hit, k, ja, p);
+    }
+};
+
+// Last task t in [lo, hi) with start(t) <= x.
+__device__ __forceinline__ uint32_t task_in(unsigned long long x, uint32_t lo, uint32_t hi,
+                                            const unsigned long long* wpre, const unsigned long long* sboff,
+                                            uint32_t CH) {
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sboff[mid / CH] + wpre[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kThreads) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
+                                                          const unsigned long long* wpre, const unsigned long long* bsum,
+                                                          uint32_t nchunks, SupportCtl* ctl) {
+    extern __shared__ uint2 tab[];
+    __shared__ unsigned long long sboff[kMaxChunks + 1];
+    __shared__ uint32_t sh_p;
+    const unsigned long long W = chunk_offsets<kThreads>(bsum, nchunks, sboff);
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->probes = W;
+    if (W == 0) return;
+    const uint32_t m = g.m, CH = chunk_len(m, nchunks);
+    const uint32_t wid = threadIdx.x >> 5;
+    unsigned long long PS = (W + 4ull * gridDim.x - 1) / (4ull * gridDim.x);
+    PS = PS < 4096 ? 4096 : PS;
+    const unsigned long long npieces = (W + PS - 1) / PS;
+    auto start = [&](uint32_t t) -> unsigned long long { return t < m ? sboff[t / CH] + wpre[t] : W; };
+    SupportPolicy SP{g, s, g.oadj};
+    while (true) {
+        if (threadIdx.x == 0) sh_p = atomicAdd(&ctl->piece_head, 1u);
+        __syncthreads();
+        const uint32_t p = sh_p;
+        __syncthreads();
+        if (p >= npieces) break;
+        const unsigned long long x0 = p * PS, x1 = x0 + PS < W ? x0 + PS : W;
+        uint32_t i = task_at(x0, m, wpre, sboff, nchunks, CH);
+        unsigned long long base = x0;
+        while (base < x1) {
+            // batch of segments searched in global memory, up to the next table segment
+            uint32_t j = i, x = 0, dp = 0, tend = 0;
+            unsigned long long bend = base, send = 0;
+            bool table = false;
+            while (bend < x1) {
+                x = g.sx[j];
+                tend = g.sbeg[x + 1];
+                send = start(tend);
+                send = send < x1 ? send : x1;
+                dp = g.opos[x + 1] - g.opos[x];
+                table = 2u * dp <= kSupTab && send - bend >= (dp > 512u ? dp : 512u);
+                if (table) break;
+                bend = send;
+                j = tend;
+            }
+            if (bend > base) {
+                const unsigned long long w0 = base + (bend - base) * wid / kSupWarps;
+                const unsigned long long w1 = base + (bend - base) * (wid + 1) / kSupWarps;
+                if (w0 < w1) run_items(SP, w0, w1, task_in(w0, i, j, wpre, sboff, CH), m, wpre, sboff, CH);
+            }
+            if (!table) break;  // bend == x1
+            // table segment: owner x, tasks [j, tend), items [bend, send)
+            uint32_t size = 64;
+            while (size < 2u * dp) size <<= 1;
+            for (uint32_t q = threadIdx.x; q < size; q += kThreads) tab[q] = make_uint2(kHEmpty, 0u);
+            __syncthreads();
+            const uint32_t o = g.opos[x];
+            for (uint32_t q = threadIdx.x; q < dp; q += kThreads) {
+                const uint32_t c = g.oadj[o + q];
+                uint32_t h = hmix(c) & (size - 1);
+                while (atomicCAS(&tab[h].x, kHEmpty, c) != kHEmpty) h = (h + 1) & (size - 1);
+                tab[h].y = q;  // position in N+(x), as the search form's find returns
+            }
+            __syncthreads();
+            SupportTabPolicy TP{g, s, g.oadj, tab, size - 1};
+            const unsigned long long w0 = bend + (send - bend) * wid / kSupWarps;
+            const unsigned long long w1 = bend + (send - bend) * (wid + 1) / kSupWarps;
+            if (w0 < w1) run_items(TP, w0, w1, task_in(w0, j, tend, wpre, sboff, CH), m, wpre, sboff, CH);
+            __syncthreads();
+            base = send;
+            i = tend;
+        }
+    }
+}
 
 __global__ void __launch_bounds__(kThreads) k_support_prep(DevGraph g, unsigned long long* wpre, unsigned long long* bsum) {
     prep_items<kThreads>(g.m, [&](uint32_t t) {
@@ -149,7 +272,22 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* w
     unsigned grid = static_cast<unsigned>(sm_count * per_sm);
     const unsigned nchunks = grid < kMaxChunks ? grid : kMaxChunks;
     k_support_prep<<<nchunks, kThreads, 0, st>>>(g, wpre, bsum);
-    k_support<<<grid, kThreads, 0, st>>>(g, s, wpre, bsum, nchunks, ctl);
+    static const bool tab_form = [] {
+        const char* e = std::getenv("TDG_SUP_FORM");  // diagnostic A/B: "search" = global search only
+        return !(e && e[0] == 's');
+    }();
+    if (tab_form) {
+        const size_t smem = size_t(kSupTab) * sizeof(uint2);
+        static const cudaError_t attr =
+            cudaFuncSetAttribute(k_support_tab, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (attr != cudaSuccess) return attr;
+        int tb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb, k_support_tab, kThreads, smem);
+        if (tb < 1) tb = 1;
+        k_support_tab<<<static_cast<unsigned>(sm_count * tb), kThreads, smem, st>>>(g, s, wpre, bsum, nchunks, ctl);
+    } else {
+        k_support<<<grid, kThreads, 0, st>>>(g, s, wpre, bsum, nchunks, ctl);
+    }
     k_support_sum<<<grid, kThreads, 0, st>>>(s, g.m, ctl);
     (*launches) += 3;
     return cudaGetLastError();

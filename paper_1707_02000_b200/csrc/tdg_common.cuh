@@ -200,6 +200,7 @@ struct DevGraph {
     const uint32_t* osrc = nullptr;
     const uint32_t* stask = nullptr;  // support tasks (slot index), see build.cu k_svalid
     const uint32_t* sx = nullptr;     // owner vertex of each support task's slot
+    const uint32_t* sbeg = nullptr;   // n+1: first support task of each owner
 };
 
 }  // namespace tdg

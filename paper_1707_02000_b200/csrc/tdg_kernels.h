@@ -28,6 +28,7 @@ struct BuildBufs {
     uint32_t* osrc;        // m
     uint32_t* stask;       // m  support tasks: slot index, grouped by searched-list owner
     uint32_t* sx;          // m  owner of that slot
+    uint32_t* sbeg;        // n+1 first support task of each owner (tasks are grouped by owner)
     void* cub_tmp;
     size_t cub_bytes;
 };
