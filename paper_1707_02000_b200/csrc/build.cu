@@ -131,6 +131,18 @@ __global__ void k_hinsert(const uint32_t* __restrict__ off, const uint32_t* __re
     }
 }
 
+// Filter bits of every slot (x -> y) whose owner table is big enough (tdg_common.cuh).
+__global__ void k_finsert(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ src,
+                          const uint32_t* __restrict__ hoff4, uint64_t slots, unsigned long long* __restrict__ filt) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t x = src[j], y = adj[j];
+        const uint32_t q0 = hoff4[x], T = 4u * (hoff4[x + 1] - q0);
+        if (T < kFMin) continue;
+        atomicOr(&filt[(q0 >> 1) + (fword(y) & (T / 8u - 1u))], fbits(hmix(y)));
+    }
+}
+
 // Support-pass task list: each oriented edge a->b is owned by the endpoint whose N+ list
 // is searched (the longer one; ties -> the source), and tasks are stored grouped by that
 // owner so consecutive tasks search the same L1-resident list. Slot j of owner x with
@@ -313,6 +325,18 @@ cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uin
     const uint64_t slots = 2ull * m;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
     k_hinsert<<<gs, kThreads, 0, st>>>(off, adj, src, eid, hoff4, slots, htab);
+    (*launches)++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_filter_fill(const uint32_t* adj, const uint32_t* src, const uint32_t* hoff4, uint32_t m,
+                               unsigned long long* filt, uint64_t filt_words, cudaStream_t st, uint32_t* launches) {
+    if (m == 0) return cudaSuccess;
+    cudaError_t err = cudaMemsetAsync(filt, 0, filt_words * sizeof(unsigned long long), st);
+    if (err != cudaSuccess) return err;
+    const uint64_t slots = 2ull * m;
+    const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
+    k_finsert<<<gs, kThreads, 0, st>>>(adj, src, hoff4, slots, filt);
     (*launches)++;
     return cudaGetLastError();
 }

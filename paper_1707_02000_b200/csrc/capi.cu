@@ -78,6 +78,10 @@ struct HostCtl {
 
 }  // namespace
 
+namespace {
+bool peel_filter();
+}  // namespace
+
 struct tdg_context {
     int device = 0;
     int sms = 148;
@@ -85,7 +89,7 @@ struct tdg_context {
     cudaStream_t stream = nullptr;
     DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx, sbeg;
     DevBuf cchunk, cscr, pbits;
-    DevBuf dl, s, stamp, L0, L1, A0, A1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab, Ls, bhist, bcur, trace;
+    DevBuf dl, s, stamp, L0, L1, A0, A1, F0, F1, X0, X1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab, filt, Ls, bhist, bcur, trace;
     DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing;
     HostCtl* hctl = nullptr;
     cudaEvent_t ev[8] = {};
@@ -127,6 +131,10 @@ struct tdg_context {
         L1.ensure(m * 4, "L1");
         A0.ensure(m * 4, "A0");
         A1.ensure(m * 4, "A1");
+        F0.ensure(m * 4, "F0");
+        F1.ensure(m * 4, "F1");
+        X0.ensure(m * 4, "X0");
+        X1.ensure(m * 4, "X1");
         Ls.ensure(m * 4, "Ls");
         if (bhist.cap == 0) {
             bhist.ensure(kBuckets * 4, "bhist");
@@ -183,6 +191,7 @@ struct tdg_context {
         g.sbeg = sbeg.as<uint32_t>();
         g.hoff4 = hoff4.as<uint32_t>();
         g.htab = htab.as<unsigned long long>();
+        g.filt = peel_filter() ? filt.as<unsigned long long>() : nullptr;
         return g;
     }
     PeelBufs peel_bufs(uint32_t n) const {
@@ -193,6 +202,10 @@ struct tdg_context {
         p.L[1] = L1.as<uint32_t>();
         p.A[0] = A0.as<uint32_t>();
         p.A[1] = A1.as<uint32_t>();
+        p.F[0] = F0.as<uint32_t>();
+        p.F[1] = F1.as<uint32_t>();
+        p.X[0] = X0.as<uint32_t>();
+        p.X[1] = X1.as<uint32_t>();
         p.wpre = src.as<unsigned long long>();  // build scratch (2m u32), free once built
         p.bsum = bsum.as<unsigned long long>();
         p.ctl = ctl.as<PeelCtl>();
@@ -223,8 +236,8 @@ struct tdg_context {
     }
     void trim() {
         DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
-                         &osrc, &stask, &sx, &sbeg, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &nsl, &ctl, &sctl, &sacc, &cub,
-                         &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &Ls, &bhist, &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1,
+                         &osrc, &stask, &sx, &sbeg, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &F0, &F1, &X0, &X1, &nsl, &ctl, &sctl, &sacc, &cub,
+                         &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &filt, &Ls, &bhist, &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1,
                          &kwpre, &kctl, &ktmp, &knoff, &knadj, &kperm, &kbad, &ing, &cchunk, &cscr, &pbits};
         for (DevBuf* b : all) b->release();
     }
@@ -338,6 +351,15 @@ Dims check_graph(const tdg_csr* g, bool host_ptrs) {
 }
 
 // Upload / alias the CSR and build eo/eid/el (+ orientation). Records ev[0], ev[1], ev[2].
+// Peel membership filters (tdg_common.cuh); TDG_PEEL_FILTER=0 disables them (A/B).
+bool peel_filter() {
+    static const bool on = [] {
+        const char* e = std::getenv("TDG_PEEL_FILTER");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // internal=true (truss / support): edge ids become oriented slots before the hash tables are
 // filled (build.cu launch_internal_ids); results go back to reference ids via oeid.
 void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, bool orient, bool tables,
@@ -371,6 +393,12 @@ void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, b
         ck(launch_htab_fill(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->src.as<uint32_t>(), c->eid.as<uint32_t>(),
                             c->hoff4.as<uint32_t>(), d.m, c->htab.as<unsigned long long>(), slots, c->stream,
                             &c->launches), "hash fill");
+        if (peel_filter()) {
+            const uint64_t words = c->hctl->htab_quads / 2 + 1;
+            c->filt.ensure(words * 8, "filters");
+            ck(launch_filter_fill(c->adj.as<uint32_t>(), c->src.as<uint32_t>(), c->hoff4.as<uint32_t>(), d.m,
+                                  c->filt.as<unsigned long long>(), words, c->stream, &c->launches), "filter fill");
+        }
     }
     ck(cudaEventRecord(c->ev[2], c->stream), "event");
 }

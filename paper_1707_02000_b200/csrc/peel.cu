@@ -52,7 +52,7 @@ constexpr int kPeelThreads = 256;
 #define TDG_PEEL_MINB 4  // min resident blocks/SM: 64 registers, 32 warps per SM
 #endif
 #ifndef TDG_PEEL_U
-#define TDG_PEEL_U 2  // probe items per lane per window step (independent chains in flight)
+#define TDG_PEEL_U 3  // probe items per lane per window step (independent chains in flight)
 #endif
 constexpr int kScanItems = 8;
 constexpr int kWarps = kPeelThreads / 32;
@@ -100,6 +100,7 @@ __device__ __forceinline__ void reset_ctr(PhaseCtr* c) {
     c->min_s = 0xffffffffu;
     c->piece_head = 0;
     c->batch_head = 0;
+    c->far_size = 0;
 }
 
 // Per-edge state packed in one 64-bit word: low half = support s[e], high half = the
@@ -119,10 +120,13 @@ __device__ __forceinline__ uint32_t st_s(unsigned long long w) { return static_c
 __device__ __forceinline__ uint32_t st_stamp(unsigned long long w) { return static_cast<uint32_t>(w >> 32); }
 
 // try_decrement, truss_parallel.cpp:49-63, with the target's support `cur` already loaded.
-// Returns target if this thread moved it to the level (it then owns the append), else kNone.
+// Returns target if this thread moved it to the level (it then owns the append), else kNone;
+// `cross` = target if this decrement took it below the near bound B (a far edge entering
+// the near range, see phase_scan), else kNone.
 __device__ __forceinline__ uint32_t try_dec(unsigned long long* ss, uint32_t cur, uint32_t level, uint32_t K,
-                                            uint32_t e1, uint32_t target, uint32_t other,
-                                            bool other_in_curr) {
+                                            uint32_t B, uint32_t e1, uint32_t target, uint32_t other,
+                                            bool other_in_curr, uint32_t& cross) {
+    cross = kNone;
     if (cur <= level) return kNone;                          // :52
     if (other_in_curr && e1 >= other) return kNone;          // :53 ownership
     const uint32_t prev = atomicSub(s_ptr(ss, target), 1u);  // :54
@@ -131,20 +135,21 @@ __device__ __forceinline__ uint32_t try_dec(unsigned long long* ss, uint32_t cur
         return target;
     }
     if (prev <= level) atomicAdd(s_ptr(ss, target), 1u);     // :58-62 repair
+    else if (prev == B) cross = target;
     return kNone;
 }
 
-// Append up to two targets per lane to next, one atomic per warp (appender.hpp:12-40).
-__device__ __forceinline__ void emit(uint32_t o0, uint32_t o1, PhaseCtr* out, uint32_t* next) {
-    const uint32_t p0 = warp_append(o0 != kNone, &out->out_size);
-    if (o0 != kNone) next[p0] = o0;
-    const uint32_t p1 = warp_append(o1 != kNone, &out->out_size);
-    if (o1 != kNone) next[p1] = o1;
+// Append up to two targets per lane to a list, one atomic per warp (appender.hpp:12-40).
+__device__ __forceinline__ void emit(uint32_t o0, uint32_t o1, uint32_t* ctr, uint32_t* list) {
+    const uint32_t p0 = warp_append(o0 != kNone, ctr);
+    if (o0 != kNone) list[p0] = o0;
+    const uint32_t p1 = warp_append(o1 != kNone, ctr);
+    if (o1 != kNone) list[p1] = o1;
 }
 
 // Append every lane's valid targets (o[j] != kNone) to next with one atomic per warp.
 template <int N>
-__device__ __forceinline__ void emit_many(const uint32_t (&o)[N], PhaseCtr* out, uint32_t* next) {
+__device__ __forceinline__ void emit_many(const uint32_t (&o)[N], uint32_t* ctr, uint32_t* next) {
     uint32_t c = 0;
 #pragma unroll
     for (int j = 0; j < N; j++) c += o[j] != kNone ? 1u : 0u;
@@ -157,7 +162,7 @@ __device__ __forceinline__ void emit_many(const uint32_t (&o)[N], PhaseCtr* out,
         if (lane >= d) incl += t;
     }
     uint32_t base = 0;
-    if (lane == 31) base = atomicAdd(&out->out_size, incl);
+    if (lane == 31) base = atomicAdd(ctr, incl);
     base = __shfl_sync(kFull, base, 31) + incl - c;
 #pragma unroll
     for (int j = 0; j < N; j++)
@@ -177,6 +182,9 @@ struct PeelPolicy {
     const uint32_t* elems;
     unsigned long long* hit_ctr;  // diagnostic, may be null
     uint32_t* stage;              // this warp's kStageB-entry shared buffer
+    uint32_t B;                   // near bound (phase_scan): decrements from B append to X
+    uint32_t* X;
+    uint32_t* xcnt;
     static constexpr bool kHasStaged = true;
     static constexpr int kUnroll = TDG_PEEL_U;
     __device__ ITask load(uint32_t t) const { return ptask(g, curr[t]); }
@@ -197,12 +205,32 @@ struct PeelPolicy {
                 ea[q] = g.eid[ko[q].oa + ja[q]];
             }
         }
+        // membership filter of a big table: a certain miss skips the table (tdg_common.cuh)
+        bool look[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            look[q] = act[q] && x[q] != ko[q].aux;
+            h[q] = look[q] ? hmix(x[q]) : 0u;
+        }
+        if (g.filt) {
+            unsigned long long fw[U];
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                fw[q] = ~0ull;
+                if (look[q] && ko[q].lb + 1u >= kFMin)
+                    fw[q] = __ldg(g.filt + (ko[q].ob >> 1) + (fword(x[q]) & ((ko[q].lb + 1u) / 8u - 1u)));
+            }
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                const unsigned long long fb = fbits(h[q]);
+                if ((fw[q] & fb) != fb) look[q] = false;
+            }
+        }
 #pragma unroll
         for (int q = 0; q < U; q++) {
             ent[q] = kHEmpty;
-            h[q] = 0;
-            if (act[q] && x[q] != ko[q].aux) {
-                h[q] = hmix(x[q]) & ko[q].lb;
+            if (look[q]) {
+                h[q] &= ko[q].lb;
                 ent[q] = g.htab[4ull * ko[q].ob + h[q]];
             }
         }
@@ -245,20 +273,24 @@ struct PeelPolicy {
 #pragma unroll
         for (int j = 0; j < 2 * U; j++)
             if (tg[j] != kNone) pv[j] = atomicSub(s_ptr(ss, tg[j]), 1u);  // :54
-        uint32_t o[2 * U];
+        uint32_t o[2 * U], c[2 * U];
 #pragma unroll
         for (int j = 0; j < 2 * U; j++) {
             o[j] = kNone;
+            c[j] = kNone;
             if (tg[j] != kNone) {
                 if (pv[j] == level + 1) {  // :55-57
                     st_relaxed(stamp_ptr(ss, tg[j]), K + 1);
                     o[j] = tg[j];
                 } else if (pv[j] <= level) {
                     atomicAdd(s_ptr(ss, tg[j]), 1u);  // :58-62 repair
+                } else if (pv[j] == B) {
+                    c[j] = tg[j];  // crossed below the near bound
                 }
             }
         }
-        emit_many(o, ph, next);
+        emit_many(o, &ph->out_size, next);
+        emit_many(c, xcnt, X);
         if (hit_ctr) {
 #pragma unroll
             for (int q = 0; q < U; q++) {
@@ -331,17 +363,18 @@ struct PeelPolicy {
         return v == kNone ? kNone : (v & ~kHUp);
     }
     __device__ void visit(bool active, bool hit, const ITask& k, uint32_t ja, uint32_t eb) const {
-        uint32_t o0 = kNone, o1 = kNone;
+        uint32_t o0 = kNone, o1 = kNone, c0 = kNone, c1 = kNone;
         if (hit) {
             const uint32_t ea = g.eid[k.oa + ja];
             const unsigned long long wa = ld_state(ss, ea), wb = ld_state(ss, eb);
             const uint32_t sa = st_stamp(wa), sb = st_stamp(wb);
-            if (!((sa != 0 && sa < K) || (sb != 0 && sb < K))) {                // :85 processed peer
-                o0 = try_dec(ss, st_s(wa), level, K, k.id, ea, eb, sb == K);  // :86
-                o1 = try_dec(ss, st_s(wb), level, K, k.id, eb, ea, sa == K);  // :87
+            if (!((sa != 0 && sa < K) || (sb != 0 && sb < K))) {                        // :85 processed peer
+                o0 = try_dec(ss, st_s(wa), level, K, B, k.id, ea, eb, sb == K, c0);  // :86
+                o1 = try_dec(ss, st_s(wb), level, K, B, k.id, eb, ea, sa == K, c1);  // :87
             }
         }
-        emit(o0, o1, ph, next);
+        emit(o0, o1, &ph->out_size, next);
+        emit(c0, c1, xcnt, X);
         if (hit_ctr) {  // diagnostics: hits, probes whose own slot is already processed
             const uint32_t hm = __ballot_sync(kFull, hit);
             bool dead = false;
@@ -358,67 +391,104 @@ struct PeelPolicy {
     }
 };
 
-// scan (truss_parallel.cpp:21-37) over the live-edge list A: survivors with s==level
-// become curr (stamp K), the others are compacted into Aout and their minimum support is
-// reduced for level skipping. Block-aggregated appends: 2 atomics per 2048 edges.
-__device__ void phase_scan(unsigned long long* ss, uint32_t level, uint32_t K, const uint32_t* Ain,
-                           uint32_t nA, bool implicit, uint32_t* Aout, uint32_t* curr, PhaseCtr* ph) {
-    __shared__ uint32_t sh_c[kWarps], sh_a[kWarps];
-    __shared__ uint32_t sh_bc, sh_ba;
+// scan (truss_parallel.cpp:21-37), near/far form. The live edges are split at a bound B:
+// the NEAR list holds those with support < B, the FAR list the rest (at split time).
+// Supports only fall, so a scan at level < B needs only the near list plus the far edges
+// whose support has since crossed below B (the process phase appends them, once, to a
+// crosser list when its atomicSub returns exactly B). When the level reaches B the far
+// list is re-split with a new bound. Each scan reads three input segments — near A, crossers
+// X, and (on a re-split) far F — and writes: s == level -> curr (stamp K); s < B -> near
+// out; else -> far out. Far entries whose support is already below the old bound are
+// dropped (they crossed and sit in A/X). Block-aggregated appends: 3 atomics per 2048 edges.
+struct ScanIn {
+    const uint32_t* A;  // near list (or implicit 0..nA-1 when implicit)
+    uint32_t nA;
+    bool implicit;
+    const uint32_t* X;  // crossers
+    uint32_t nX;
+    const uint32_t* F;  // far list (re-split scans only)
+    uint32_t nF;
+    uint32_t Bold;      // bound the far list was split at
+    uint32_t B;         // bound of the outputs
+};
+
+__device__ void phase_scan(unsigned long long* ss, uint32_t level, uint32_t K, const ScanIn in, uint32_t* Aout,
+                           uint32_t* Fout, uint32_t* curr, PhaseCtr* ph) {
+    __shared__ uint32_t sh_c[kWarps], sh_a[kWarps], sh_f[kWarps];
+    __shared__ uint32_t sh_bc, sh_ba, sh_bf;
     const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
     const uint64_t tile = uint64_t(kPeelThreads) * kScanItems;
+    const uint64_t nAX = uint64_t(in.nA) + in.nX, ntot = nAX + in.nF;
     uint32_t local_min = 0xffffffffu;
-    for (uint64_t t0 = uint64_t(blockIdx.x) * tile; t0 < nA; t0 += uint64_t(gridDim.x) * tile) {
+    for (uint64_t t0 = uint64_t(blockIdx.x) * tile; t0 < ntot; t0 += uint64_t(gridDim.x) * tile) {
         uint32_t es[kScanItems];
-        uint32_t kind = 0;  // 2 bits per item: 1 = curr, 2 = alive
-        uint32_t cc = 0, ca = 0;
+        uint32_t kind = 0;  // 2 bits per item: 1 = curr, 2 = near, 3 = far
+        uint32_t cc = 0, ca = 0, cf = 0;
 #pragma unroll
         for (int k = 0; k < kScanItems; k++) {
             const uint64_t i = t0 + uint64_t(k) * kPeelThreads + tid;
             es[k] = 0;
-            if (i < nA) {
-                const uint32_t e = implicit ? static_cast<uint32_t>(i) : Ain[i];
+            if (i < ntot) {
+                const bool far_in = i >= nAX;
+                const uint32_t e = i < in.nA ? (in.implicit ? static_cast<uint32_t>(i) : in.A[i])
+                                             : (far_in ? in.F[i - nAX] : in.X[i - in.nA]);
                 es[k] = e;
                 const unsigned long long w = ld_state(ss, e);
-                if (st_stamp(w) == 0) {
-                    const uint32_t sv = st_s(w);
+                const uint32_t sv = st_s(w);
+                if (st_stamp(w) == 0 && !(far_in && sv < in.Bold)) {
                     if (sv == level) {
                         st_relaxed(stamp_ptr(ss, e), K);
                         kind |= 1u << (2 * k);
                         cc++;
-                    } else {
+                    } else if (sv < in.B) {
                         kind |= 2u << (2 * k);
                         ca++;
                         local_min = sv < local_min ? sv : local_min;
+                    } else {
+                        kind |= 3u << (2 * k);
+                        cf++;
                     }
                 }
             }
         }
-        const uint32_t ic = warp_incl_scan(cc), ia = warp_incl_scan(ca);
-        if (lane == 31) { sh_c[wid] = ic; sh_a[wid] = ia; }
+        const uint32_t ic = warp_incl_scan(cc), ia = warp_incl_scan(ca), iff = warp_incl_scan(cf);
+        if (lane == 31) { sh_c[wid] = ic; sh_a[wid] = ia; sh_f[wid] = iff; }
         __syncthreads();
         if (tid == 0) {
-            uint32_t rc = 0, ra = 0;
+            uint32_t rc = 0, ra = 0, rf = 0;
             for (int w = 0; w < kWarps; w++) {
-                uint32_t c = sh_c[w], a = sh_a[w];
-                sh_c[w] = rc; sh_a[w] = ra;
-                rc += c; ra += a;
+                const uint32_t c = sh_c[w], a = sh_a[w], f = sh_f[w];
+                sh_c[w] = rc; sh_a[w] = ra; sh_f[w] = rf;
+                rc += c; ra += a; rf += f;
             }
             sh_bc = rc ? atomicAdd(&ph->out_size, rc) : 0;
             sh_ba = ra ? atomicAdd(&ph->alive_size, ra) : 0;
+            sh_bf = rf ? atomicAdd(&ph->far_size, rf) : 0;
         }
         __syncthreads();
-        uint32_t pc = sh_bc + sh_c[wid] + ic - cc, pa = sh_ba + sh_a[wid] + ia - ca;
+        uint32_t pc = sh_bc + sh_c[wid] + ic - cc, pa = sh_ba + sh_a[wid] + ia - ca, pf = sh_bf + sh_f[wid] + iff - cf;
 #pragma unroll
         for (int k = 0; k < kScanItems; k++) {
             const uint32_t f = (kind >> (2 * k)) & 3u;
             if (f == 1u) curr[pc++] = es[k];
             else if (f == 2u) Aout[pa++] = es[k];
+            else if (f == 3u) Fout[pf++] = es[k];
         }
         __syncthreads();
     }
     for (int o = 16; o > 0; o >>= 1) local_min = min(local_min, __shfl_xor_sync(kFull, local_min, o));
     if (lane == 0 && local_min != 0xffffffffu) atomicMin(&ph->min_s, local_min);
+}
+
+// Near bound after a (re-)split at `level`: the window grows with the level so the number
+// of far re-splits stays logarithmic in t_max.
+#ifndef TDG_NEAR_ADD
+#define TDG_NEAR_ADD 8
+#define TDG_NEAR_DIV 4
+#endif
+__device__ __forceinline__ uint32_t near_bound(uint32_t level) {
+    const unsigned long long b = static_cast<unsigned long long>(level) + TDG_NEAR_ADD + level / TDG_NEAR_DIV;
+    return b > 0xfffffff0ull ? 0xfffffff0u : static_cast<uint32_t>(b);
 }
 
 // Sub-level prep: block b owns curr chunk b; probe count of e1 = min live degree.
@@ -515,10 +585,10 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             uint32_t K, const uint32_t* curr, uint32_t cs,
                                             const unsigned long long* wpre, const unsigned long long* bsum,
                                             uint32_t nchunks, PhaseCtr* ph, uint32_t* next,
-                                            unsigned long long* hit_ctr) {
+                                            unsigned long long* hit_ctr, uint32_t B, uint32_t* X, uint32_t* xcnt) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     __shared__ uint32_t sstage[kWarps * kStageB];
-    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB};
+    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB, B, X, xcnt};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }
 
@@ -694,14 +764,25 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
     PeelCtl* ctl = pb.ctl;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m;
+    uint32_t B = 0, fi = 1, nF = 0, xp = 0;  // near bound, far list parity/size, crosser parity
     bool implicit = true;
     unsigned long long t_prev = leader ? gtimer() : 0;
     unsigned long long sub_w = 0;
     const uint32_t nchunks = vload(&ctl->nchunks);
     while (true) {
-        // ---- scan at `level` (one grid barrier)
-        if (leader) { reset_ctr(&ctl->ph[(j + 1) % 3]); ctl->scans++; }
-        phase_scan(pb.ss, level, K, pb.A[ai], nA, implicit, pb.A[ai ^ 1], pb.L[li], &ctl->ph[j % 3]);
+        // ---- scan at `level` (one grid barrier); re-split the far list once level >= B
+        const bool resplit = implicit || level >= B;
+        ScanIn in{pb.A[ai], nA, implicit, pb.X[xp], vload(&ctl->xcnt[xp]), pb.F[fi], resplit ? nF : 0u, B, B};
+        if (resplit) in.B = near_bound(level);
+        if (leader) {
+            reset_ctr(&ctl->ph[(j + 1) % 3]);
+            ctl->scans++;
+            ctl->xcnt[xp ^ 1] = 0;  // crossers after this scan (read by the previous scan)
+            if (resplit) ctl->rebuilds++;
+        }
+        // (every counter read after a barrier lives in the rotating phase slots, which are
+        // reset two phases after they are written, so no block can observe a reset early)
+        phase_scan(pb.ss, level, K, in, pb.A[ai ^ 1], pb.F[fi ^ 1], pb.L[li], &ctl->ph[j % 3]);
         grid.sync();
         if (leader) { const unsigned long long t = gtimer(); ctl->scan_ns += t - t_prev; t_prev = t; }
         j++;
@@ -710,15 +791,25 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         nA = vload(&r->alive_size);
         const uint32_t mins = vload(&r->min_s);
         ai ^= 1;
+        xp ^= 1;
         implicit = false;
+        B = in.B;
+        if (resplit) {
+            fi ^= 1;
+            nF = vload(&r->far_size);
+        }
         if (cs == 0) {
-            if (nA == 0) break;
-            level = mins;  // skip empty levels
+            if (nA == 0) {
+                if (nF == 0) break;
+                level = B;  // only far edges are left, all with support >= B
+            } else {
+                level = mins;  // skip empty levels
+            }
             continue;
         }
         // ---- compaction once the live edge count fell below kCompactFrac of the last one
-        if (level > 0 && (static_cast<unsigned long long>(cs) + nA) * kCompactDen <
-                             static_cast<unsigned long long>(live_at_compact) * kCompactNum) {
+        const unsigned long long live = static_cast<unsigned long long>(cs) + nA + nF;
+        if (level > 0 && live * kCompactDen < static_cast<unsigned long long>(live_at_compact) * kCompactNum) {
             if (leader) { reset_ctr(&ctl->ph[(j + 1) % 3]); ctl->compactions++; }
             phase_compact_long(g, pb.ss, K, pb, nchunks);
             phase_compact_short(g, pb.pbits);
@@ -727,7 +818,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             grid.sync();
             if (leader) { const unsigned long long t = gtimer(); ctl->compact_ns += t - t_prev; }
             j++;
-            live_at_compact = cs + nA;
+            live_at_compact = static_cast<uint32_t>(live);
         }
         // ---- sub-levels: prep + process (two grid barriers each; level 0 one)
         while (true) {
@@ -755,7 +846,8 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                 grid.sync();
                 const unsigned long long W =
                     phase_process(g, pb.ss, level, K, tasks, cs, pb.wpre, pb.bsum, gridDim.x,
-                                  &ctl->ph[j % 3], pb.L[li ^ 1], pb.count_hits ? &ctl->hits : nullptr);
+                                  &ctl->ph[j % 3], pb.L[li ^ 1], pb.count_hits ? &ctl->hits : nullptr, B,
+                                  pb.X[xp], &ctl->xcnt[xp]);
                 if (leader) {
                     ctl->probes += W;
                     sub_w = W;
@@ -832,7 +924,8 @@ __global__ void k_step_stamps(const uint8_t* __restrict__ processed, const uint8
 }
 
 __global__ void __launch_bounds__(kPeelThreads) k_step_scan(PeelBufs pb, uint32_t m, uint32_t level) {
-    phase_scan(pb.ss, level, 2, pb.A[0], m, true, pb.A[1], pb.L[0], &pb.ctl->ph[0]);
+    const ScanIn in{pb.A[0], m, true, nullptr, 0u, nullptr, 0u, 0u, 0xffffffffu};  // one near list, no far
+    phase_scan(pb.ss, level, 2, in, pb.A[1], pb.A[1], pb.L[0], &pb.ctl->ph[0]);
 }
 
 __global__ void k_step_scan_flags(const uint32_t* __restrict__ curr, PeelCtl* ctl, uint8_t* in_curr) {
@@ -849,7 +942,7 @@ __global__ void __launch_bounds__(kPeelThreads) k_step_prep(DevGraph g, PeelBufs
 __global__ void __launch_bounds__(kPeelThreads) k_step_process(DevGraph g, PeelBufs pb, uint32_t cs, uint32_t level,
                                                                uint32_t nchunks) {
     phase_process(g, pb.ss, level, 2, pb.L[0], cs, pb.wpre, pb.bsum, nchunks, &pb.ctl->ph[1], pb.L[1],
-                  nullptr);
+                  nullptr, 0xffffffffu, nullptr, &pb.ctl->xcnt[0]);
 }
 
 // Epilogue (truss_parallel.cpp:97-102) + in_next flags for the appended edges; unpacks s.

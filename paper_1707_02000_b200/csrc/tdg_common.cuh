@@ -185,10 +185,33 @@ __device__ __forceinline__ uint32_t hlookup(const unsigned long long* __restrict
     }
 }
 
+// ---- per-vertex membership filters (register-blocked Bloom filters) in front of the big
+// tables. A table of T >= kFMin slots owns T/8 64-bit words at word offset hoff4/2 (its
+// quad offset halved: big tables have an even quad count, so regions never overlap) —
+// >= 16 bits per key. A key sets 3 bits of one word; a lookup whose bits are not all set
+// is a certain miss and skips the table walk. The filter is 1/8 of the table's bytes, so
+// the misses of a sub-level (~3/4 of all probes) mostly hit L2 instead of DRAM.
+#ifndef TDG_FMIN
+#define TDG_FMIN 1024
+#endif
+constexpr uint32_t kFMin = TDG_FMIN;
+
+__device__ __forceinline__ uint32_t fword(uint32_t x) {
+    x = (x ^ 0x9e3779b9u) * 0x85ebca6bu;
+    x ^= x >> 15;
+    x *= 0xc2b2ae35u;
+    x ^= x >> 13;
+    return x;
+}
+__device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(key)
+    return (1ull << ((h >> 14) & 63)) | (1ull << ((h >> 20) & 63)) | (1ull << ((h >> 26) & 63));
+}
+
 struct DevGraph {
     uint32_t n = 0, m = 0;
     const uint32_t* hoff4 = nullptr;          // n+1, table offsets in units of 4 slots
     const unsigned long long* htab = nullptr;  // hash table slots
+    const unsigned long long* filt = nullptr;  // membership filters of the big tables (or null)
     const uint32_t* off = nullptr;
     uint32_t* adj = nullptr;
     uint32_t* eid = nullptr;

@@ -52,6 +52,10 @@ cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uin
                              const uint32_t* hoff4, uint32_t m, unsigned long long* htab, uint64_t htab_slots,
                              cudaStream_t st, uint32_t* launches);
 
+// Membership filters of the big tables (tdg_common.cuh); filt_words = htab quads / 2 + 1.
+cudaError_t launch_filter_fill(const uint32_t* adj, const uint32_t* src, const uint32_t* hoff4, uint32_t m,
+                               unsigned long long* filt, uint64_t filt_words, cudaStream_t st, uint32_t* launches);
+
 struct StatsAcc {
     unsigned long long d_max, sum_deg_sq, sum_dplus_sq, deg_sum_dplus_sq, deg_s1;
 };
@@ -133,7 +137,7 @@ struct PhaseCtr {
     uint32_t min_s;          // scan: min support over survivors (level skipping)
     uint32_t piece_head;     // sub-level: dynamic piece cursor
     uint32_t batch_head;     // sub-level / scan: dynamic batch cursor
-    uint32_t pad;
+    uint32_t far_size;       // scan: far-list appends (peel.cu near/far scan)
 };
 struct PeelCtl {
     PhaseCtr ph[3];
@@ -151,6 +155,9 @@ struct PeelCtl {
     unsigned long long hits;     // triangle visits (only when PeelBufs::count_hits)
     unsigned long long dead;     // probes whose own slot was already processed (diagnostic)
     unsigned long long compact_ns;  // device-clock time in adjacency compactions
+    uint32_t xcnt[2];  // crosser-list append counters (peel.cu near/far scan)
+    uint32_t rebuilds;  // scans that re-split the far list
+    uint32_t pad2;
 };
 struct PeelBufs {
     uint32_t* s;               // support (u32): input of the peel / step-function I/O
@@ -177,6 +184,8 @@ struct PeelBufs {
     uint32_t* sadj;
     uint32_t* seid;
     uint32_t* pbits;  // (m+31)/32 words: bit e set once edge e's sub-level has run
+    uint32_t* F[2];   // m each: far live edges (support >= the near bound when split)
+    uint32_t* X[2];   // m each: far edges whose support crossed below the near bound
 };
 constexpr uint32_t kBuckets = 1u << 16;
 // Whole level loop in one persistent cooperative launch.

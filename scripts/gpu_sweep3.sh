@@ -12,3 +12,6 @@ for v in "${VS[@]}"; do
   for c in ${CONFIGS:-3 5}; do echo "== $name C$c"; timeout 600 python scripts/run_one.py $c 2 2>&1 | summ; done
 done
 touch paper_1707_02000_b200/csrc/peel.cu; make -s -C paper_1707_02000_b200/csrc -j16 2>&1 | grep error
+touch paper_1707_02000_b200/csrc/support.cu; make -s -C paper_1707_02000_b200/csrc -j16 NVEXTRA=-DTDG_SUP_TAB=2048 2>&1 | grep error
+for c in ${CONFIGS:-3 5}; do echo "== suptab2048 C$c"; timeout 600 python scripts/run_one.py $c 2 2>&1 | summ; done
+touch paper_1707_02000_b200/csrc/support.cu; make -s -C paper_1707_02000_b200/csrc -j16 2>&1 | grep error
