@@ -6,13 +6,15 @@
 //   eo[u]   = first slot of u with neighbour > u                    (graph.cpp:80-84)
 //   P       = exclusive scan of up[u] = off[u+1]-eo[u]              (edge-id base per u)
 //   upper slot j of u (v>u): eid = P[u] + j - eo[u], el[eid] = (u,v)
-//   lower slot j of u (v<u): eid = P[v] + lower_bound(adj[eo[v]..off[v+1]), u)
+//   lower slot j of u (v<u): the mirror's id, read from the upper-slot ids stably sorted by
+//                            upper endpoint (a transpose; position j - P[u], k_eid_lower)
 // Then the support pass's orientation (north-star item 1): u->v iff
 // (d(u),u) < (d(v),v); the oriented lists are order-preserving subsequences of adj,
 // compacted with one global scan of per-slot flags. All passes are slot-parallel
-// (load-balanced regardless of degree skew) and HBM-streaming except the lower-slot
-// binary search.
+// (load-balanced regardless of degree skew) and HBM-streaming plus one radix sort of m
+// (key, id) pairs.
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "tdg_kernels.h"
@@ -54,26 +56,41 @@ __global__ void k_eo(const uint32_t* __restrict__ off, const uint32_t* __restric
     }
 }
 
+// Upper slot j of u (v > u): eid = P[u] + j - eo[u], el[eid] = (u,v); the pair (v, eid) is
+// emitted for the transpose below. Lower slots are filled by k_eid_lower.
 __global__ void k_eid(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
                       const uint32_t* __restrict__ src, const uint32_t* __restrict__ eo,
                       const uint32_t* __restrict__ P, uint64_t slots, uint32_t* __restrict__ eid,
-                      uint2* __restrict__ el, uint32_t* __restrict__ flag) {
+                      uint2* __restrict__ el, uint32_t* __restrict__ flag, uint32_t* __restrict__ tkey,
+                      uint32_t* __restrict__ tval) {
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t u = src[j], v = adj[j];
-        uint32_t e;
         if (v > u) {
-            e = P[u] + static_cast<uint32_t>(j - eo[u]);
+            const uint32_t e = P[u] + static_cast<uint32_t>(j - eo[u]);
             el[e] = make_uint2(u, v);
-        } else {
-            const uint32_t lo = eo[v];
-            e = P[v] + lower_bound_u32(adj + lo, off[v + 1] - lo, u);
+            eid[j] = e;
+            tkey[e] = v;
+            tval[e] = e;
         }
-        eid[j] = e;
         if (flag) {
             const uint32_t du = off[u + 1] - off[u], dv = off[v + 1] - off[v];
             flag[j] = (du < dv || (du == dv && u < v)) ? 1u : 0u;
         }
+    }
+}
+
+// Lower slot j of u (v < u). The edge ids sorted (stably) by upper endpoint list, for each
+// u, the ids of its edges (v,u), v < u, in ascending v — exactly u's lower slots in order.
+// u's group starts at off[u] - P[u] (lower slots of the vertices before u), so slot j
+// reads position j - P[u]. Replaces a binary search in N(v) per lower slot.
+__global__ void k_eid_lower(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ src,
+                            const uint32_t* __restrict__ P, const uint32_t* __restrict__ sorted_ids, uint64_t slots,
+                            uint32_t* __restrict__ eid) {
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t u = src[j];
+        if (adj[j] < u) eid[j] = sorted_ids[j - P[u]];
     }
 }
 
@@ -243,6 +260,10 @@ size_t build_cub_bytes(uint32_t n, uint32_t m) {
                                   static_cast<uint64_t>(n) + 1);
     cub::DeviceScan::ExclusiveSum(nullptr, c, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
                                   slots + 1);
+    size_t d = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, d, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                    static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), m > 0 ? m : 1);
+    c = c > d ? c : d;
     size_t r = a > b ? a : b;
     return r > c ? r : c;
 }
@@ -266,9 +287,16 @@ cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_o
     err = cub::DeviceScan::ExclusiveSum(b.cub_tmp, tmp, b.up, b.P, static_cast<uint64_t>(n) + 1, st);
     if (err != cudaSuccess) return err;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
+    // transpose scratch: the orientation arrays are free until k_orient
     k_eid<<<gs, kThreads, 0, st>>>(b.off, b.adj, b.src, b.eo, b.P, slots, b.eid, b.el,
-                                   with_orientation ? b.flag : nullptr);
-    (*launches)++;
+                                   with_orientation ? b.flag : nullptr, b.oadj, b.oeid);
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < n) bits++;
+    tmp = b.cub_bytes;
+    err = cub::DeviceRadixSort::SortPairs(b.cub_tmp, tmp, b.oadj, b.osrc, b.oeid, b.stask, m, 0, bits, st);
+    if (err != cudaSuccess) return err;
+    k_eid_lower<<<gs, kThreads, 0, st>>>(b.adj, b.src, b.P, b.stask, slots, b.eid);
+    (*launches) += 2;
     if (!with_orientation) return cudaGetLastError();
     if ((err = cudaMemsetAsync(b.flag + slots, 0, sizeof(uint32_t), st)) != cudaSuccess) return err;
     tmp = b.cub_bytes;

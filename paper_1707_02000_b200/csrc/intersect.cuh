@@ -129,6 +129,10 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
     uint32_t held = kNone;
     ITask k{0, 0, 0, 0, 0, kNone};
     unsigned long long st = ~0ull, end_held = ~0ull;
+    // fast-path cache: lane 0's task broadcast to every lane, valid while i == c_task
+    ITask c0{0, 0, 0, 0, 0, kNone};
+    unsigned long long c_st = 0;
+    uint32_t c_task = kNone;
     for (unsigned long long base = x0; base < x1;) {
         if (held != i) {
             // Slide the held window: tasks already held move down by `adv` lanes with
@@ -183,27 +187,45 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
         const uint32_t relk = st <= base ? 0u
                               : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
         constexpr int U = Policy::kUnroll;
+        // Fast path (Policy::kFast): when lane 0's task covers the whole step (the next task
+        // starts at least 32U items on), every item belongs to it and its descriptor, broadcast
+        // once, is reused while the warp stays inside it — no per-item owner search. (The
+        // peel's U = 3 probe loop is register-bound and loses more to the cache than it saves.)
+        const uint32_t r1 = Policy::kFast ? __shfl_sync(kFull, relk, 1) : 0u;
+        const bool one = Policy::kFast && r1 >= 32u * U;
         if constexpr (U > 1) {
             // U items per lane per step (item base + lane + 32q): the policy issues their
             // independent loads together, so each lane keeps U probe chains in flight.
             ITask ko[U];
             uint32_t ja[U];
             bool act[U];
+            if (one) {
+                if (c_task != i) { c0 = shfl_task(k, 0); c_st = shfl64(st, 0); c_task = i; }
 #pragma unroll
-            for (int q = 0; q < U; q++) {
-                const uint32_t key = lane + 32u * q;
-                const uint32_t own = warp_search_le(relk, key);
-                const unsigned long long so = shfl64(st, own);
-                ko[q] = shfl_task(k, own);
-                const unsigned long long x = base + key;
-                act[q] = x < limit;
-                ja[q] = act[q] ? static_cast<uint32_t>(x - so) : 0u;
+                for (int q = 0; q < U; q++) {
+                    const unsigned long long x = base + lane + 32u * q;
+                    ko[q] = c0;
+                    act[q] = x < limit;
+                    ja[q] = act[q] ? static_cast<uint32_t>(x - c_st) : 0u;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < U; q++) {
+                    const uint32_t key = lane + 32u * q;
+                    const uint32_t own = warp_search_le(relk, key);
+                    const unsigned long long so = shfl64(st, own);
+                    ko[q] = shfl_task(k, own);
+                    const unsigned long long x = base + key;
+                    act[q] = x < limit;
+                    ja[q] = act[q] ? static_cast<uint32_t>(x - so) : 0u;
+                }
             }
             P.template run<U>(act, ko, ja);
         } else {
-            const uint32_t own = warp_search_le(relk, lane);
-            const unsigned long long so = shfl64(st, own);
-            const ITask ko = shfl_task(k, own);
+            if (one && c_task != i) { c0 = shfl_task(k, 0); c_st = shfl64(st, 0); c_task = i; }
+            const uint32_t own = one ? 0u : warp_search_le(relk, lane);
+            const unsigned long long so = one ? c_st : shfl64(st, own);
+            const ITask ko = one ? c0 : shfl_task(k, own);
             const unsigned long long x = base + lane;
             uint32_t ja = 0, e = kNone;
             const bool active = x < limit;
@@ -214,7 +236,9 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
             P.visit(active, e != kNone, ko, ja, e);
         }
         const unsigned long long nb = base + 32u * U < limit ? base + 32u * U : limit;
-        i = (nb >= end_held) ? i + 32 : i + warp_search_le(relk, static_cast<uint32_t>(nb - base));
+        i = (nb >= end_held) ? i + 32
+            : (one && nb - base < r1) ? i  // still inside lane 0's task
+                                      : i + warp_search_le(relk, static_cast<uint32_t>(nb - base));
         base = nb;
     }
 }

@@ -51,6 +51,7 @@ struct KcorePolicy {
     uint32_t* next;
     const uint32_t* elems;
     static constexpr bool kHasStaged = false;
+    static constexpr bool kFast = false;
     static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const {
         const uint32_t v = curr[t];

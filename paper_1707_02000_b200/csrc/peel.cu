@@ -186,6 +186,7 @@ struct PeelPolicy {
     uint32_t* X;
     uint32_t* xcnt;
     static constexpr bool kHasStaged = true;
+    static constexpr bool kFast = false;
     static constexpr int kUnroll = TDG_PEEL_U;
     __device__ ITask load(uint32_t t) const { return ptask(g, curr[t]); }
     __device__ bool staged(const ITask& k) const { return (k.lb & kStaged) != 0; }

@@ -49,6 +49,7 @@ struct SupportPolicy {
     uint32_t* s;
     const uint32_t* elems;
     static constexpr bool kHasStaged = false;
+    static constexpr bool kFast = true;
     static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ bool staged(const ITask&) const { return false; }
@@ -93,6 +94,7 @@ struct SupportTabPolicy {
     const uint2* tab;
     uint32_t mask;
     static constexpr bool kHasStaged = false;
+    static constexpr bool kFast = true;
     static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ bool staged(const ITask&) const { return false; }
@@ -207,6 +209,7 @@ struct CountPolicy {
     const uint32_t* elems;
     unsigned long long count = 0;
     static constexpr bool kHasStaged = false;
+    static constexpr bool kFast = true;
     static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ bool staged(const ITask&) const { return false; }
