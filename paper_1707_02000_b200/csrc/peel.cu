@@ -52,7 +52,7 @@ constexpr int kPeelThreads = 256;
 #define TDG_PEEL_MINB 4  // min resident blocks/SM: 64 registers, 32 warps per SM
 #endif
 #ifndef TDG_PEEL_U
-#define TDG_PEEL_U 3  // probe items per lane per window step (independent chains in flight)
+#define TDG_PEEL_U 2  // probe items per lane per window step (independent chains in flight)
 #endif
 constexpr int kScanItems = 8;
 constexpr int kWarps = kPeelThreads / 32;
@@ -64,7 +64,7 @@ constexpr int kWarps = kPeelThreads / 32;
 //    the piece's slice of N(b) is staged in shared memory and searched there (PeelPolicy).
 constexpr uint32_t kStaged = 0x80000000u;
 #ifndef TDG_STAGE_MIN
-#define TDG_STAGE_MIN 512  // probe-list length from which a task may be staged
+#define TDG_STAGE_MIN 0  // probe-list length from which a task may be staged (0 = off: measured faster with the filters)
 #endif
 #ifndef TDG_STAGE_RATIO
 #define TDG_STAGE_RATIO 8  // ... if the searched list is at most this many times longer
@@ -185,7 +185,7 @@ struct PeelPolicy {
     uint32_t B;                   // near bound (phase_scan): decrements from B append to X
     uint32_t* X;
     uint32_t* xcnt;
-    static constexpr bool kHasStaged = true;
+    static constexpr bool kHasStaged = TDG_STAGE_MIN != 0;
     static constexpr bool kFast = false;
     static constexpr int kUnroll = TDG_PEEL_U;
     __device__ ITask load(uint32_t t) const { return ptask(g, curr[t]); }

@@ -44,19 +44,34 @@ __device__ __forceinline__ ITask otask(const DevGraph& g, uint32_t t) {
 // L2-resident N+(x) range and the probe-side slots of one task are consecutive, so the
 // per-triangle atomics stay out of DRAM (reference-id-indexed atomics were random 2 GB
 // read-modify-writes at C5).
+#ifndef TDG_SUP_U
+#define TDG_SUP_U 2  // probe items per lane per engine step in the support pass
+#endif
 struct SupportPolicy {
     const DevGraph& g;
     uint32_t* s;
     const uint32_t* elems;
     static constexpr bool kHasStaged = false;
     static constexpr bool kFast = true;
-    static constexpr int kUnroll = 1;
+    static constexpr int kUnroll = TDG_SUP_U;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ bool staged(const ITask&) const { return false; }
     __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
     __device__ uint32_t find(const ITask& k, uint32_t x) const {
         const uint32_t p = lower_bound_u32(g.oadj + k.ob, k.lb, x);
         return (p < k.lb && g.oadj[k.ob + p] == x) ? p : kNone;
+    }
+    // U items per lane per engine step: the U list loads and lookups issue together and
+    // the engine's per-step bookkeeping is amortised over 32U probes.
+    template <int U>
+    __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
+        uint32_t c[U], p[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) c[q] = act[q] ? elems[ko[q].oa + ja[q]] : 0u;
+#pragma unroll
+        for (int q = 0; q < U; q++) p[q] = act[q] ? find(ko[q], c[q]) : kNone;
+#pragma unroll
+        for (int q = 0; q < U; q++) visit(act[q], p[q] != kNone, ko[q], ja[q], p[q]);
     }
     // A hit closes triangle {x, y, c}: the oriented slots of y->c and x->c get one atomic
     // each, the task's edge one per group of lanes sharing it (__match_any_sync).
@@ -66,9 +81,16 @@ struct SupportPolicy {
             atomicAdd(&s[k.ob + p], 1u);
         }
         const uint32_t fm = __ballot_sync(kFull, hit);
-        if (fm && hit) {
-            const uint32_t grp = __match_any_sync(fm, k.id);
-            if (lane_id() == static_cast<uint32_t>(__ffs(grp) - 1)) atomicAdd(&s[k.id], static_cast<uint32_t>(__popc(grp)));
+        if (fm) {
+            // usually every hitting lane works on the same task: one ballot instead of a match
+            const uint32_t first = __ffs(fm) - 1;
+            const uint32_t id0 = __shfl_sync(kFull, k.id, first);
+            if (__all_sync(kFull, !hit || k.id == id0)) {
+                if (lane_id() == first) atomicAdd(&s[id0], static_cast<uint32_t>(__popc(fm)));
+            } else if (hit) {
+                const uint32_t grp = __match_any_sync(fm, k.id);
+                if (lane_id() == static_cast<uint32_t>(__ffs(grp) - 1)) atomicAdd(&s[k.id], static_cast<uint32_t>(__popc(grp)));
+            }
         }
     }
 };
@@ -82,7 +104,7 @@ struct SupportPolicy {
 // are too small to pay for the table, or whose owner list exceeds the table, are batched
 // and searched in global memory as before.
 #ifndef TDG_SUP_TAB
-#define TDG_SUP_TAB 4096  // shared-memory table slots (8 B each): owners with d+ <= TAB/2
+#define TDG_SUP_TAB 4096  // shared-memory table slots (8 B each): owners with d+ <= 3/4 TAB
 #endif
 constexpr uint32_t kSupTab = TDG_SUP_TAB;
 constexpr uint32_t kSupWarps = kThreads / 32;
@@ -95,7 +117,7 @@ struct SupportTabPolicy {
     uint32_t mask;
     static constexpr bool kHasStaged = false;
     static constexpr bool kFast = true;
-    static constexpr int kUnroll = 1;
+    static constexpr int kUnroll = TDG_SUP_U;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ bool staged(const ITask&) const { return false; }
     __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
@@ -107,6 +129,18 @@ struct SupportTabPolicy {
             if (e.x == kHEmpty) return kNone;
             h = (h + 1) & mask;
         }
+    }
+    // U items per lane per engine step: the U list loads and lookups issue together and
+    // the engine's per-step bookkeeping is amortised over 32U probes.
+    template <int U>
+    __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
+        uint32_t c[U], p[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) c[q] = act[q] ? elems[ko[q].oa + ja[q]] : 0u;
+#pragma unroll
+        for (int q = 0; q < U; q++) p[q] = act[q] ? find(ko[q], c[q]) : kNone;
+#pragma unroll
+        for (int q = 0; q < U; q++) visit(act[q], p[q] != kNone, ko[q], ja[q], p[q]);
     }
     __device__ void visit(bool a, bool hit, const ITask& k, uint32_t ja, uint32_t p) const {
         SupportPolicy{g, s, elems}.visit(a, hit, k, ja, p);
@@ -160,7 +194,7 @@ __global__ void __launch_bounds__(kThreads) k_support_tab(DevGraph g, uint32_t* 
                 send = start(tend);
                 send = send < x1 ? send : x1;
                 dp = g.opos[x + 1] - g.opos[x];
-                table = 2u * dp <= kSupTab && send - bend >= (dp > 512u ? dp : 512u);
+                table = 4u * dp <= 3u * kSupTab && send - bend >= (dp > 512u ? dp : 512u);
                 if (table) break;
                 bend = send;
                 j = tend;
@@ -173,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) k_support_tab(DevGraph g, uint32_t* 
             if (!table) break;  // bend == x1
             // table segment: owner x, tasks [j, tend), items [bend, send)
             uint32_t size = 64;
-            while (size < 2u * dp) size <<= 1;
+            while (size < 2u * dp && size < kSupTab) size <<= 1;  // load <= 1/2, or <= 3/4 when full size
             for (uint32_t q = threadIdx.x; q < size; q += kThreads) tab[q] = make_uint2(kHEmpty, 0u);
             __syncthreads();
             const uint32_t o = g.opos[x];
