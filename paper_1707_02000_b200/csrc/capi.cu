@@ -391,10 +391,10 @@ void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, b
         const uint64_t slots = 4ull * c->hctl->htab_quads;
         c->htab.ensure(slots * 8, "hash tables");
         ck(launch_htab_fill(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->src.as<uint32_t>(), c->eid.as<uint32_t>(),
-                            c->hoff4.as<uint32_t>(), d.m, c->htab.as<unsigned long long>(), slots, c->stream,
+                            c->hoff4.as<uint32_t>(), d.n, d.m, c->htab.as<unsigned long long>(), slots, c->stream,
                             &c->launches), "hash fill");
         if (peel_filter()) {
-            const uint64_t words = c->hctl->htab_quads / 2 + 1;
+            const uint64_t words = (c->hctl->htab_quads >> kFShift) + 1;
             c->filt.ensure(words * 8, "filters");
             ck(launch_filter_fill(c->adj.as<uint32_t>(), c->src.as<uint32_t>(), c->hoff4.as<uint32_t>(), d.m,
                                   c->filt.as<unsigned long long>(), words, c->stream, &c->launches), "filter fill");

@@ -219,7 +219,7 @@ struct PeelPolicy {
             for (int q = 0; q < U; q++) {
                 fw[q] = ~0ull;
                 if (look[q] && ko[q].lb + 1u >= kFMin)
-                    fw[q] = __ldg(g.filt + (ko[q].ob >> 1) + (fword(x[q]) & ((ko[q].lb + 1u) / 8u - 1u)));
+                    fw[q] = __ldg(g.filt + (ko[q].ob >> kFShift) + (fword(x[q]) & (((ko[q].lb + 1u) >> (kFShift + 2)) - 1u)));
             }
 #pragma unroll
             for (int q = 0; q < U; q++) {

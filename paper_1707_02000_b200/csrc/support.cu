@@ -109,6 +109,13 @@ struct SupportPolicy {
 constexpr uint32_t kSupTab = TDG_SUP_TAB;
 constexpr uint32_t kSupWarps = kThreads / 32;
 
+// Shared-memory table slot of key c: multiplicative (Fibonacci) hashing, top bits of
+// c * 2^32/phi — one multiply and a shift instead of hmix's five-step mix (the support pass
+// is issue-bound).
+__device__ __forceinline__ uint32_t tab_hash(uint32_t c, uint32_t mask) {
+    return (c * 0x9E3779B1u) >> (__clz(mask) & 31u);
+}
+
 struct SupportTabPolicy {
     const DevGraph& g;
     uint32_t* s;
@@ -122,7 +129,7 @@ struct SupportTabPolicy {
     __device__ bool staged(const ITask&) const { return false; }
     __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
     __device__ uint32_t find(const ITask&, uint32_t c) const {
-        uint32_t h = hmix(c) & mask;
+        uint32_t h = tab_hash(c, mask);
         while (true) {
             const uint2 e = tab[h];
             if (e.x == c) return e.y;
@@ -213,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_support_tab(DevGraph g, uint32_t* 
             const uint32_t o = g.opos[x];
             for (uint32_t q = threadIdx.x; q < dp; q += kThreads) {
                 const uint32_t c = g.oadj[o + q];
-                uint32_t h = hmix(c) & (size - 1);
+                uint32_t h = tab_hash(c, size - 1);
                 while (atomicCAS(&tab[h].x, kHEmpty, c) != kHEmpty) h = (h + 1) & (size - 1);
                 tab[h].y = q;  // position in N+(x), as the search form's find returns
             }

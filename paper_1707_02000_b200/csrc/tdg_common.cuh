@@ -186,15 +186,22 @@ __device__ __forceinline__ uint32_t hlookup(const unsigned long long* __restrict
 }
 
 // ---- per-vertex membership filters (register-blocked Bloom filters) in front of the big
-// tables. A table of T >= kFMin slots owns T/8 64-bit words at word offset hoff4/2 (its
-// quad offset halved: big tables have an even quad count, so regions never overlap) —
-// >= 16 bits per key. A key sets 3 bits of one word; a lookup whose bits are not all set
+// tables. A table of T >= kFMin slots owns T/2^(kFShift+2) 64-bit words at word offset
+// hoff4 >> kFShift (big tables have quad counts divisible by 2^kFShift, so regions never
+// overlap) — >= 32/2^kFShift bits per key. A key sets 3 bits of one word; a lookup whose bits are not all set
 // is a certain miss and skips the table walk. The filter is 1/8 of the table's bytes, so
 // the misses of a sub-level (~3/4 of all probes) mostly hit L2 instead of DRAM.
 #ifndef TDG_FMIN
 #define TDG_FMIN 1024
 #endif
 constexpr uint32_t kFMin = TDG_FMIN;
+#ifndef TDG_FSHIFT
+#define TDG_FSHIFT 3  // 4 bits per key: sparser filters stay L2-resident (C5: 16 -> 8 -> 4 bits, 3.47 -> 3.26 -> 3.19 s)
+#endif
+#ifndef TDG_FK
+#define TDG_FK 3  // bits set per key
+#endif
+constexpr uint32_t kFShift = TDG_FSHIFT;
 
 __device__ __forceinline__ uint32_t fword(uint32_t x) {
     x = (x ^ 0x9e3779b9u) * 0x85ebca6bu;
@@ -204,7 +211,9 @@ __device__ __forceinline__ uint32_t fword(uint32_t x) {
     return x;
 }
 __device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(key)
-    return (1ull << ((h >> 14) & 63)) | (1ull << ((h >> 20) & 63)) | (1ull << ((h >> 26) & 63));
+    unsigned long long b = (1ull << ((h >> 14) & 63)) | (1ull << ((h >> 20) & 63));
+    if (TDG_FK > 2) b |= 1ull << ((h >> 26) & 63);
+    return b;
 }
 
 struct DevGraph {

@@ -49,7 +49,7 @@ cudaError_t launch_to_ref(const uint32_t* oeid, const uint32_t* in, uint32_t m, 
 cudaError_t launch_htab_sizes(const uint32_t* off, uint32_t n, uint32_t* hq, uint32_t* hoff4, void* cub_tmp,
                               size_t cub_bytes, cudaStream_t st, uint32_t* launches);
 cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, const uint32_t* eid,
-                             const uint32_t* hoff4, uint32_t m, unsigned long long* htab, uint64_t htab_slots,
+                             const uint32_t* hoff4, uint32_t n, uint32_t m, unsigned long long* htab, uint64_t htab_slots,
                              cudaStream_t st, uint32_t* launches);
 
 // Membership filters of the big tables (tdg_common.cuh); filt_words = htab quads / 2 + 1.
