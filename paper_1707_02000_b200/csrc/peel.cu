@@ -185,6 +185,7 @@ struct PeelPolicy {
     uint32_t B;                   // near bound (phase_scan): decrements from B append to X
     uint32_t* X;
     uint32_t* xcnt;
+    const uint32_t* pbits;        // edges processed in earlier sub-levels (or null)
     static constexpr bool kHasStaged = TDG_STAGE_MIN != 0;
     static constexpr bool kFast = false;
     static constexpr int kUnroll = TDG_PEEL_U;
@@ -213,6 +214,11 @@ struct PeelPolicy {
             look[q] = act[q] && x[q] != ko[q].aux;
             h[q] = look[q] ? hmix(x[q]) : 0u;
         }
+        // ... and so does an own slot already processed in an earlier sub-level (:85): its
+        // bit (L2-resident bitmap, consecutive lanes share words) is read beside the filter
+        uint32_t pw[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) pw[q] = (pbits && look[q]) ? pbits[ea[q] >> 5] : 0u;
         if (g.filt) {
             unsigned long long fw[U];
 #pragma unroll
@@ -227,6 +233,9 @@ struct PeelPolicy {
                 if ((fw[q] & fb) != fb) look[q] = false;
             }
         }
+#pragma unroll
+        for (int q = 0; q < U; q++)
+            if ((pw[q] >> (ea[q] & 31u)) & 1u) look[q] = false;
 #pragma unroll
         for (int q = 0; q < U; q++) {
             ent[q] = kHEmpty;
@@ -586,10 +595,11 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             uint32_t K, const uint32_t* curr, uint32_t cs,
                                             const unsigned long long* wpre, const unsigned long long* bsum,
                                             uint32_t nchunks, PhaseCtr* ph, uint32_t* next,
-                                            unsigned long long* hit_ctr, uint32_t B, uint32_t* X, uint32_t* xcnt) {
+                                            unsigned long long* hit_ctr, uint32_t B, uint32_t* X, uint32_t* xcnt,
+                                            const uint32_t* pbits) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     __shared__ uint32_t sstage[kWarps * kStageB];
-    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB, B, X, xcnt};
+    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB, B, X, xcnt, pbits};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }
 
@@ -766,6 +776,8 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m;
     uint32_t B = 0, fi = 1, nF = 0, xp = 0;  // near bound, far list parity/size, crosser parity
+    const uint32_t* pend = nullptr;          // last sub-level's curr, not yet in pbits
+    uint32_t pend_n = 0;
     bool implicit = true;
     unsigned long long t_prev = leader ? gtimer() : 0;
     unsigned long long sub_w = 0;
@@ -783,6 +795,8 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         }
         // (every counter read after a barrier lives in the rotating phase slots, which are
         // reset two phases after they are written, so no block can observe a reset early)
+        if (pend_n) mark_processed(pb.pbits, pend, pend_n);  // before the compaction that may follow
+        pend_n = 0;
         phase_scan(pb.ss, level, K, in, pb.A[ai ^ 1], pb.F[fi ^ 1], pb.L[li], &ctl->ph[j % 3]);
         grid.sync();
         if (leader) { const unsigned long long t = gtimer(); ctl->scan_ns += t - t_prev; t_prev = t; }
@@ -829,9 +843,9 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                 ctl->levels_len = level + 1;
                 reset_ctr(&ctl->ph[(j + 1) % 3]);
             }
-            // curr's edges are processed once this sub-level ends; the bits are read only by
-            // the next compaction (after at least one more grid barrier)
-            mark_processed(pb.pbits, pb.L[li], cs);
+            // the previous sub-level's curr is processed now: mark it (read by this sub-level's
+            // probes and by compaction; this sub-level's own curr is marked by the next phase)
+            if (pend_n) mark_processed(pb.pbits, pend, pend_n);
             if (level > 0) {  // level 0: s[e1] == 0 bounds its live triangles to none
                 const uint32_t* tasks = pb.L[li];
                 if (kSortMin && cs >= kSortMin) {  // group big sub-levels by searched vertex
@@ -848,7 +862,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                 const unsigned long long W =
                     phase_process(g, pb.ss, level, K, tasks, cs, pb.wpre, pb.bsum, gridDim.x,
                                   &ctl->ph[j % 3], pb.L[li ^ 1], pb.count_hits ? &ctl->hits : nullptr, B,
-                                  pb.X[xp], &ctl->xcnt[xp]);
+                                  pb.X[xp], &ctl->xcnt[xp], pb.pbits);
                 if (leader) {
                     ctl->probes += W;
                     sub_w = W;
@@ -871,6 +885,8 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             j++;
             K++;
             r = &ctl->ph[(j - 1) % 3];
+            pend = pb.L[li];
+            pend_n = cs;
             cs = vload(&r->out_size);
             li ^= 1;
             if (cs == 0) break;
@@ -943,7 +959,7 @@ __global__ void __launch_bounds__(kPeelThreads) k_step_prep(DevGraph g, PeelBufs
 __global__ void __launch_bounds__(kPeelThreads) k_step_process(DevGraph g, PeelBufs pb, uint32_t cs, uint32_t level,
                                                                uint32_t nchunks) {
     phase_process(g, pb.ss, level, 2, pb.L[0], cs, pb.wpre, pb.bsum, nchunks, &pb.ctl->ph[1], pb.L[1],
-                  nullptr, 0xffffffffu, nullptr, &pb.ctl->xcnt[0]);
+                  nullptr, 0xffffffffu, nullptr, &pb.ctl->xcnt[0], nullptr);
 }
 
 // Epilogue (truss_parallel.cpp:97-102) + in_next flags for the appended edges; unpacks s.

@@ -107,6 +107,12 @@ struct SupportPolicy {
 #define TDG_SUP_TAB 4096  // shared-memory table slots (8 B each): owners with d+ <= 3/4 TAB
 #endif
 constexpr uint32_t kSupTab = TDG_SUP_TAB;
+#ifndef TDG_SUP_LOAD
+#define TDG_SUP_LOAD 2  // table slots per key when the table is not full size (most probes miss)
+#endif
+#ifndef TDG_SUP_MINB
+#define TDG_SUP_MINB 1
+#endif
 constexpr uint32_t kSupWarps = kThreads / 32;
 
 // Shared-memory table slot of key c: multiplicative (Fibonacci) hashing, top bits of
@@ -165,7 +171,7 @@ __device__ __forceinline__ uint32_t task_in(unsigned long long x, uint32_t lo, u
     return lo;
 }
 
-__global__ void __launch_bounds__(kThreads) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
+__global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
                                                           const unsigned long long* wpre, const unsigned long long* bsum,
                                                           uint32_t nchunks, SupportCtl* ctl) {
     extern __shared__ uint2 tab[];
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_support_tab(DevGraph g, uint32_t* 
             if (!table) break;  // bend == x1
             // table segment: owner x, tasks [j, tend), items [bend, send)
             uint32_t size = 64;
-            while (size < 2u * dp && size < kSupTab) size <<= 1;  // load <= 1/2, or <= 3/4 when full size
+            while (size < TDG_SUP_LOAD * dp && size < kSupTab) size <<= 1;  // load <= 1/LOAD, or <= 3/4 at full size
             for (uint32_t q = threadIdx.x; q < size; q += kThreads) tab[q] = make_uint2(kHEmpty, 0u);
             __syncthreads();
             const uint32_t o = g.opos[x];
