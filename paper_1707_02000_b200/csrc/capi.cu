@@ -218,7 +218,7 @@ struct tdg_context {
         p.bcur = bcur.as<uint32_t>();
         uint32_t bits = 0;
         while ((1ull << bits) < n) bits++;
-        p.bshift = bits > 16 ? bits - 16 : 0;
+        p.bshift = bits > kBucketBits ? bits - kBucketBits : 0;
         p.trace = nullptr;
         p.trace_cap = 0;
         if (std::getenv("TDG_TRACE")) {

@@ -243,6 +243,10 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
     }
 }
 
+#ifndef TDG_PIECES
+#define TDG_PIECES 4ull  // work pieces per warp in process_items (dynamic; smaller = shorter tail)
+#endif
+
 // sboff[c] = exclusive prefix of the chunk totals bsum[0..nchunks) (block-wide; smem
 // sboff holds >= nchunks+1 entries); returns the total work.
 template <int kThreads>
@@ -274,7 +278,7 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
     if (W == 0) return 0;
     const uint32_t CH = chunk_len(ntasks, nchunks);
     const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
-    unsigned long long PS = (W + 4ull * nwarps - 1) / (4ull * nwarps);
+    unsigned long long PS = (W + TDG_PIECES * nwarps - 1) / (TDG_PIECES * nwarps);
     PS = (PS + 31) & ~31ull;
     if (PS < 32) PS = 32;
     const unsigned long long npieces = (W + PS - 1) / PS;

@@ -47,7 +47,10 @@ namespace tdg {
 
 namespace {
 
-constexpr int kPeelThreads = 256;
+#ifndef TDG_PEEL_THREADS
+#define TDG_PEEL_THREADS 256
+#endif
+constexpr int kPeelThreads = TDG_PEEL_THREADS;
 #ifndef TDG_PEEL_MINB
 #define TDG_PEEL_MINB 4  // min resident blocks/SM: 64 registers, 32 warps per SM
 #endif
@@ -598,7 +601,7 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             unsigned long long* hit_ctr, uint32_t B, uint32_t* X, uint32_t* xcnt,
                                             const uint32_t* pbits) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
-    __shared__ uint32_t sstage[kWarps * kStageB];
+    __shared__ uint32_t sstage[TDG_STAGE_MIN ? kWarps * kStageB : 1];
     PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB, B, X, xcnt, pbits};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }

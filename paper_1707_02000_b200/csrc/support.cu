@@ -110,6 +110,12 @@ constexpr uint32_t kSupTab = TDG_SUP_TAB;
 #ifndef TDG_SUP_LOAD
 #define TDG_SUP_LOAD 4  // table slots per key when the table is not full size (most probes miss)
 #endif
+#ifndef TDG_SUP_SEGMIN
+#define TDG_SUP_SEGMIN 512u  // a segment gets a table if its probes * SEGDIV >= max(d+(x), SEGMIN)
+#endif
+#ifndef TDG_SUP_SEGDIV
+#define TDG_SUP_SEGDIV 1u
+#endif
 #ifndef TDG_SUP_MINB
 #define TDG_SUP_MINB 5  // 5 blocks/SM (shared memory allows 5; C5 support 1.39 -> 1.20 s)
 #endif
@@ -207,7 +213,8 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
                 send = start(tend);
                 send = send < x1 ? send : x1;
                 dp = g.opos[x + 1] - g.opos[x];
-                table = 4u * dp <= 3u * kSupTab && send - bend >= (dp > 512u ? dp : 512u);
+                table = 4u * dp <= 3u * kSupTab &&
+                        (send - bend) * TDG_SUP_SEGDIV >= (dp > TDG_SUP_SEGMIN ? dp : TDG_SUP_SEGMIN);
                 if (table) break;
                 bend = send;
                 j = tend;

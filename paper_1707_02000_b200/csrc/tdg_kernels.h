@@ -187,7 +187,11 @@ struct PeelBufs {
     uint32_t* F[2];   // m each: far live edges (support >= the near bound when split)
     uint32_t* X[2];   // m each: far edges whose support crossed below the near bound
 };
-constexpr uint32_t kBuckets = 1u << 16;
+#ifndef TDG_BUCKET_BITS
+#define TDG_BUCKET_BITS 16
+#endif
+constexpr uint32_t kBucketBits = TDG_BUCKET_BITS;
+constexpr uint32_t kBuckets = 1u << kBucketBits;
 // Whole level loop in one persistent cooperative launch.
 cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cudaStream_t st,
                         uint32_t* launches);
