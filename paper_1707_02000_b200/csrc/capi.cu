@@ -231,6 +231,9 @@ struct tdg_context {
         p.ckept = reinterpret_cast<uint32_t*>(p.chunks + cc);
         p.sadj = cscr.as<uint32_t>();
         p.seid = p.sadj ? p.sadj + cscr.cap / 8 : nullptr;
+        // sub-level task descriptors share the compaction scratch (m x 16 B): compaction runs
+        // only between a scan and the first sub-level of a level
+        p.desc = cscr.as<uint4>();
         p.pbits = pbits.as<uint32_t>();
         return p;
     }

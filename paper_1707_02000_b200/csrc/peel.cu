@@ -72,6 +72,7 @@ constexpr uint32_t kStaged = 0x80000000u;
 #ifndef TDG_STAGE_RATIO
 #define TDG_STAGE_RATIO 8  // ... if the searched list is at most this many times longer
 #endif
+constexpr bool kDesc = TDG_STAGE_MIN == 0;  // task descriptors from prep (phase_prep)
 constexpr uint32_t kStageA = 128;  // probe elements per staged chunk
 constexpr uint32_t kStageB = 768;  // max searched-list slice held in shared memory (per warp)
 
@@ -189,10 +190,17 @@ struct PeelPolicy {
     uint32_t* X;
     uint32_t* xcnt;
     const uint32_t* pbits;        // edges processed in earlier sub-levels (or null)
+    const uint4* desc;            // task descriptors written by phase_prep (or null)
     static constexpr bool kHasStaged = TDG_STAGE_MIN != 0;
     static constexpr bool kFast = false;
     static constexpr int kUnroll = TDG_PEEL_U;
-    __device__ ITask load(uint32_t t) const { return ptask(g, curr[t]); }
+    __device__ ITask load(uint32_t t) const {
+        if (kDesc && desc) {  // (aux = kNone: b's own id never occurs in its table, only a filter miss is lost)
+            const uint4 d = desc[t];
+            return ITask{curr[t], d.x, d.y, d.z, d.w, kNone};
+        }
+        return ptask(g, curr[t]);
+    }
     __device__ bool staged(const ITask& k) const { return (k.lb & kStaged) != 0; }
     // U hash-form probes per lane, stage by stage so the U chains' loads overlap:
     // list element + its edge id (coalesced) -> first table slot -> (collisions) ->
@@ -573,9 +581,19 @@ __device__ void phase_bucket_scatter(const DevGraph& g, const uint32_t* curr, ui
     }
 }
 
+// Task descriptors: prep resolves each task's three levels of dependent random loads
+// (el -> dl -> off / table offset) once and stores {oa, la, ob, lb} in task order, so the
+// process phase's window refills are one coalesced 16-byte load per lane (the descriptor
+// loads were ~8 % of the peel's stall samples). Not used with staging (its tasks need aux).
+
 __device__ void phase_prep(const DevGraph& g, const uint32_t* curr, uint32_t cs, unsigned long long* wpre,
-                           unsigned long long* bsum) {
+                           unsigned long long* bsum, uint4* desc) {
     prep_items<kPeelThreads>(cs, [&](uint32_t t) {
+        if (kDesc && desc) {
+            const ITask k = ptask(g, curr[t]);
+            desc[t] = make_uint4(k.oa, k.la, k.ob, k.lb);
+            return k.la;
+        }
         const uint2 p = g.el[curr[t]];
         return min(g.dl[p.x], g.dl[p.y]);
     }, wpre, bsum);
@@ -599,10 +617,10 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             const unsigned long long* wpre, const unsigned long long* bsum,
                                             uint32_t nchunks, PhaseCtr* ph, uint32_t* next,
                                             unsigned long long* hit_ctr, uint32_t B, uint32_t* X, uint32_t* xcnt,
-                                            const uint32_t* pbits) {
+                                            const uint32_t* pbits, const uint4* desc) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     __shared__ uint32_t sstage[TDG_STAGE_MIN ? kWarps * kStageB : 1];
-    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB, B, X, xcnt, pbits};
+    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB, B, X, xcnt, pbits, desc};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }
 
@@ -860,12 +878,12 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                     grid.sync();
                     tasks = pb.Ls;
                 }
-                phase_prep(g, tasks, cs, pb.wpre, pb.bsum);
+                phase_prep(g, tasks, cs, pb.wpre, pb.bsum, pb.desc);
                 grid.sync();
                 const unsigned long long W =
                     phase_process(g, pb.ss, level, K, tasks, cs, pb.wpre, pb.bsum, gridDim.x,
                                   &ctl->ph[j % 3], pb.L[li ^ 1], pb.count_hits ? &ctl->hits : nullptr, B,
-                                  pb.X[xp], &ctl->xcnt[xp], pb.pbits);
+                                  pb.X[xp], &ctl->xcnt[xp], pb.pbits, pb.desc);
                 if (leader) {
                     ctl->probes += W;
                     sub_w = W;
@@ -955,14 +973,14 @@ __global__ void k_step_scan_flags(const uint32_t* __restrict__ curr, PeelCtl* ct
 }
 
 __global__ void __launch_bounds__(kPeelThreads) k_step_prep(DevGraph g, PeelBufs pb, uint32_t cs) {
-    phase_prep(g, pb.L[0], cs, pb.wpre, pb.bsum);
+    phase_prep(g, pb.L[0], cs, pb.wpre, pb.bsum, pb.desc);
 }
 
 // Hand-built states may break the level-0 invariant, so the step form always probes.
 __global__ void __launch_bounds__(kPeelThreads) k_step_process(DevGraph g, PeelBufs pb, uint32_t cs, uint32_t level,
                                                                uint32_t nchunks) {
     phase_process(g, pb.ss, level, 2, pb.L[0], cs, pb.wpre, pb.bsum, nchunks, &pb.ctl->ph[1], pb.L[1],
-                  nullptr, 0xffffffffu, nullptr, &pb.ctl->xcnt[0], nullptr);
+                  nullptr, 0xffffffffu, nullptr, &pb.ctl->xcnt[0], nullptr, pb.desc);
 }
 
 // Epilogue (truss_parallel.cpp:97-102) + in_next flags for the appended edges; unpacks s.

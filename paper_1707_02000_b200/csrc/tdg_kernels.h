@@ -186,6 +186,7 @@ struct PeelBufs {
     uint32_t* pbits;  // (m+31)/32 words: bit e set once edge e's sub-level has run
     uint32_t* F[2];   // m each: far live edges (support >= the near bound when split)
     uint32_t* X[2];   // m each: far edges whose support crossed below the near bound
+    uint4* desc;      // m: per-sub-level task descriptors (aliases the compaction scratch)
 };
 #ifndef TDG_BUCKET_BITS
 #define TDG_BUCKET_BITS 16
