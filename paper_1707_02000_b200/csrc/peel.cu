@@ -55,7 +55,7 @@ constexpr int kPeelThreads = TDG_PEEL_THREADS;
 #define TDG_PEEL_MINB 4  // min resident blocks/SM: 64 registers, 32 warps per SM
 #endif
 #ifndef TDG_PEEL_U
-#define TDG_PEEL_U 2  // probe items per lane per window step (independent chains in flight)
+#define TDG_PEEL_U 3  // probe items per lane per window step (independent chains in flight)
 #endif
 constexpr int kScanItems = 8;
 constexpr int kWarps = kPeelThreads / 32;

@@ -44,6 +44,43 @@ __device__ __forceinline__ ITask otask(const DevGraph& g, uint32_t t) {
 // L2-resident N+(x) range and the probe-side slots of one task are consecutive, so the
 // per-triangle atomics stay out of DRAM (reference-id-indexed atomics were random 2 GB
 // read-modify-writes at C5).
+// Hits of one engine step (U items per lane): each hit closes triangle {x, y, c} — the
+// oriented slots of y->c and x->c get one atomic each; the tasks' own edges are counted
+// with one atomic per step when every lane works on the same task (the common case in
+// long lists), else per item with one atomic per group of lanes sharing a task.
+template <int U>
+__device__ __forceinline__ void visit_all(uint32_t* s, const ITask (&ko)[U], const uint32_t (&ja)[U],
+                                          const uint32_t (&p)[U]) {
+    uint32_t tot = 0;
+    bool same = true;
+    const uint32_t id0 = __shfl_sync(kFull, ko[0].id, 0);
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+        const bool hit = p[q] != kNone;
+        if (hit) {
+            atomicAdd(&s[ko[q].oa + ja[q]], 1u);
+            atomicAdd(&s[ko[q].ob + p[q]], 1u);
+        }
+        tot += __popc(__ballot_sync(kFull, hit));
+        same = same && (!hit || ko[q].id == id0);
+    }
+    if (tot == 0) return;
+    if (__all_sync(kFull, same)) {
+        if (lane_id() == 0) atomicAdd(&s[id0], tot);
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+        const bool hit = p[q] != kNone;
+        const uint32_t fm = __ballot_sync(kFull, hit);
+        if (fm && hit) {
+            const uint32_t grp = __match_any_sync(fm, ko[q].id);
+            if (lane_id() == static_cast<uint32_t>(__ffs(grp) - 1))
+                atomicAdd(&s[ko[q].id], static_cast<uint32_t>(__popc(grp)));
+        }
+    }
+}
+
 #ifndef TDG_SUP_U
 #define TDG_SUP_U 2  // probe items per lane per engine step in the support pass
 #endif
@@ -70,8 +107,7 @@ struct SupportPolicy {
         for (int q = 0; q < U; q++) c[q] = act[q] ? elems[ko[q].oa + ja[q]] : 0u;
 #pragma unroll
         for (int q = 0; q < U; q++) p[q] = act[q] ? find(ko[q], c[q]) : kNone;
-#pragma unroll
-        for (int q = 0; q < U; q++) visit(act[q], p[q] != kNone, ko[q], ja[q], p[q]);
+        visit_all<U>(s, ko, ja, p);
     }
     // A hit closes triangle {x, y, c}: the oriented slots of y->c and x->c get one atomic
     // each, the task's edge one per group of lanes sharing it (__match_any_sync).
@@ -158,8 +194,7 @@ struct SupportTabPolicy {
         for (int q = 0; q < U; q++) c[q] = act[q] ? elems[ko[q].oa + ja[q]] : 0u;
 #pragma unroll
         for (int q = 0; q < U; q++) p[q] = act[q] ? find(ko[q], c[q]) : kNone;
-#pragma unroll
-        for (int q = 0; q < U; q++) visit(act[q], p[q] != kNone, ko[q], ja[q], p[q]);
+        visit_all<U>(s, ko, ja, p);
     }
     __device__ void visit(bool a, bool hit, const ITask& k, uint32_t ja, uint32_t p) const {
         SupportPolicy{g, s, elems}.visit(a, hit, k, ja, p);
