@@ -138,9 +138,11 @@ __device__ __forceinline__ unsigned long long htab_entry(const uint32_t* __restr
     return (static_cast<unsigned long long>(e | (up ? kHUp : 0u)) << 32) | y;
 }
 
-// Tables of at most kHSmall slots are built in shared memory, one warp per vertex, and
-// written out with coalesced stores (random global CAS inserts were 1.8 % of a C5 step).
+// Tables of at most kHSmall slots are built in shared memory, one warp per vertex (up to kHMid,
+// one block per vertex), and written out with coalesced stores (random global CAS inserts were
+// 1.8 % of a C5 step).
 constexpr uint32_t kHSmall = 1024;
+constexpr uint32_t kHMid = 8 * kHSmall;  // block-built tables use the block's whole 64 KB
 
 __global__ void __launch_bounds__(256) k_hbuild_small(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                       const uint32_t* __restrict__ eid, const uint32_t* __restrict__ hoff4,
@@ -165,6 +167,37 @@ __global__ void __launch_bounds__(256) k_hbuild_small(const uint32_t* __restrict
         for (uint32_t i = lane; i < T; i += 32) g[i] = t[i];
         __syncwarp();
     }
+    // Tables of kHSmall < T <= kHMid slots: the whole block builds one at a time in the same
+    // shared memory. Each block takes 256-vertex chunks and queues their mid-size tables.
+    __shared__ uint32_t q[256];
+    __shared__ uint32_t qn;
+    for (uint64_t c0 = uint64_t(blockIdx.x) * 256; c0 < n; c0 += uint64_t(gridDim.x) * 256) {
+        if (threadIdx.x == 0) qn = 0;
+        __syncthreads();
+        const uint64_t x = c0 + threadIdx.x;
+        if (x < n) {
+            const uint32_t T = 4u * (hoff4[x + 1] - hoff4[x]);
+            if (T > kHSmall && T <= kHMid) q[atomicAdd(&qn, 1u)] = static_cast<uint32_t>(x);
+        }
+        __syncthreads();
+        const uint32_t cnt = qn;
+        for (uint32_t k = 0; k < cnt; k++) {
+            const uint32_t v = q[k], q0 = hoff4[v], T = 4u * (hoff4[v + 1] - q0);
+            for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) htab_smem[i] = ~0ull;
+            __syncthreads();
+            const uint32_t o = off[v], d = off[v + 1] - o;
+            for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+                const uint32_t y = adj[o + i];
+                const unsigned long long entry = htab_entry(off, v, y, eid[o + i]);
+                uint32_t h = hmix(y) & (T - 1u);
+                while (atomicCAS(&htab_smem[h], ~0ull, entry) != ~0ull) h = (h + 1) & (T - 1u);
+            }
+            __syncthreads();
+            unsigned long long* g = htab + 4ull * q0;
+            for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) g[i] = htab_smem[i];
+            __syncthreads();
+        }
+    }
 }
 
 // Insert every slot (x -> y, eid) of a big table into x's table; the value carries the
@@ -175,7 +208,7 @@ __global__ void k_hinsert(const uint32_t* __restrict__ off, const uint32_t* __re
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t x = src[j], y = adj[j];
-        if (4u * (hoff4[x + 1] - hoff4[x]) <= kHSmall) continue;
+        if (4u * (hoff4[x + 1] - hoff4[x]) <= kHMid) continue;
         const uint32_t dx = off[x + 1] - off[x], dy = off[y + 1] - off[y];
         const bool up = dx < dy || (dx == dy && x < y);
         const unsigned long long entry = (static_cast<unsigned long long>(eid[j] | (up ? kHUp : 0u)) << 32) | y;
