@@ -66,6 +66,9 @@ constexpr int kWarps = kPeelThreads / 32;
 //  * STAGED (both lists long and of comparable length): ob = off[b], lb = dl[b] | kStaged;
 //    the piece's slice of N(b) is staged in shared memory and searched there (PeelPolicy).
 constexpr uint32_t kStaged = 0x80000000u;
+#ifndef TDG_PEEL_FAST
+#define TDG_PEEL_FAST 0  // engine fast path (intersect.cuh) for the peel's probe loop
+#endif
 #ifndef TDG_STAGE_MIN
 #define TDG_STAGE_MIN 0  // probe-list length from which a task may be staged (0 = off: measured faster with the filters)
 #endif
@@ -192,7 +195,7 @@ struct PeelPolicy {
     const uint32_t* pbits;        // edges processed in earlier sub-levels (or null)
     const uint4* desc;            // task descriptors written by phase_prep (or null)
     static constexpr bool kHasStaged = TDG_STAGE_MIN != 0;
-    static constexpr bool kFast = false;
+    static constexpr bool kFast = TDG_PEEL_FAST;
     static constexpr int kUnroll = TDG_PEEL_U;
     __device__ ITask load(uint32_t t) const {
         if (kDesc && desc) {  // (aux = kNone: b's own id never occurs in its table, only a filter miss is lost)
