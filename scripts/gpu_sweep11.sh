@@ -8,7 +8,7 @@ for l in sys.stdin:
 IFS=';' read -ra VS <<< "${VARIANTS:-load2:;load4:-DTDG_SUP_LOAD=4;load4m5:-DTDG_SUP_LOAD=4 -DTDG_SUP_MINB=5;load2m5:-DTDG_SUP_MINB=5}"
 for v in "${VS[@]}"; do
   name="${v%%:*}"; flags="${v#*:}"
-  touch paper_1707_02000_b200/csrc/support.cu paper_1707_02000_b200/csrc/peel.cu paper_1707_02000_b200/csrc/capi.cu; make -s -C paper_1707_02000_b200/csrc -j16 NVEXTRA="$flags" 2>&1 | grep -E "error"
+  touch paper_1707_02000_b200/csrc/*.cu; make -s -C paper_1707_02000_b200/csrc -j16 NVEXTRA="$flags" 2>&1 | grep -E "error"
   for c in ${CONFIGS:-3 5}; do echo "== $name C$c"; timeout 240 python scripts/run_one.py $c 2 2>&1 | summ; done
 done
-touch paper_1707_02000_b200/csrc/support.cu paper_1707_02000_b200/csrc/peel.cu paper_1707_02000_b200/csrc/capi.cu; make -s -C paper_1707_02000_b200/csrc -j16 2>&1 | grep error
+touch paper_1707_02000_b200/csrc/*.cu; make -s -C paper_1707_02000_b200/csrc -j16 2>&1 | grep error
