@@ -66,6 +66,9 @@ constexpr int kWarps = kPeelThreads / 32;
 //  * STAGED (both lists long and of comparable length): ob = off[b], lb = dl[b] | kStaged;
 //    the piece's slice of N(b) is staged in shared memory and searched there (PeelPolicy).
 constexpr uint32_t kStaged = 0x80000000u;
+#ifndef TDG_HTAB_NC
+#define TDG_HTAB_NC 0  // table slots through the read-only (non-coherent) path: tables never change in the peel
+#endif
 #ifndef TDG_PEEL_FAST
 #define TDG_PEEL_FAST 0  // engine fast path (intersect.cuh) for the peel's probe loop
 #endif
@@ -255,7 +258,7 @@ struct PeelPolicy {
             ent[q] = kHEmpty;
             if (look[q]) {
                 h[q] &= ko[q].lb;
-                ent[q] = g.htab[4ull * ko[q].ob + h[q]];
+                ent[q] = TDG_HTAB_NC ? __ldg(g.htab + 4ull * ko[q].ob + h[q]) : g.htab[4ull * ko[q].ob + h[q]];
             }
         }
 #pragma unroll
@@ -264,7 +267,7 @@ struct PeelPolicy {
             uint32_t hh = h[q];
             while (static_cast<uint32_t>(e) != kHEmpty && static_cast<uint32_t>(e) != x[q]) {
                 hh = (hh + 1) & ko[q].lb;
-                e = g.htab[4ull * ko[q].ob + hh];
+                e = TDG_HTAB_NC ? __ldg(g.htab + 4ull * ko[q].ob + hh) : g.htab[4ull * ko[q].ob + hh];
             }
             eb[q] = (x[q] != kHEmpty && static_cast<uint32_t>(e) == x[q]) ? (static_cast<uint32_t>(e >> 32) & ~kHUp)
                                                                            : kNone;
