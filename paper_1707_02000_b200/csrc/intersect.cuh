@@ -243,6 +243,9 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
     }
 }
 
+#ifndef TDG_MIN_PIECE
+#define TDG_MIN_PIECE 32ull  // smallest piece (items): bounds per-piece overhead in small phases
+#endif
 #ifndef TDG_PIECES
 #define TDG_PIECES 4ull  // work pieces per warp in process_items (dynamic; smaller = shorter tail)
 #endif
@@ -280,7 +283,7 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
     const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
     unsigned long long PS = (W + TDG_PIECES * nwarps - 1) / (TDG_PIECES * nwarps);
     PS = (PS + 31) & ~31ull;
-    if (PS < 32) PS = 32;
+    if (PS < TDG_MIN_PIECE) PS = TDG_MIN_PIECE;
     const unsigned long long npieces = (W + PS - 1) / PS;
     const uint32_t lane = lane_id();
 
