@@ -243,6 +243,9 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
     }
 }
 
+#ifndef TDG_PIECE_ROUND
+#define TDG_PIECE_ROUND 1  // round pieces to whole 32*U-item steps
+#endif
 #ifndef TDG_MIN_PIECE
 #define TDG_MIN_PIECE 32ull  // smallest piece (items): bounds per-piece overhead in small phases
 #endif
@@ -282,7 +285,8 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
     const uint32_t CH = chunk_len(ntasks, nchunks);
     const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
     unsigned long long PS = (W + TDG_PIECES * nwarps - 1) / (TDG_PIECES * nwarps);
-    PS = (PS + 31) & ~31ull;
+    constexpr unsigned long long kStep = TDG_PIECE_ROUND ? 32ull * Policy::kUnroll : 32ull;
+    PS = (PS + kStep - 1) / kStep * kStep;  // whole engine steps per piece
     if (PS < TDG_MIN_PIECE) PS = TDG_MIN_PIECE;
     const unsigned long long npieces = (W + PS - 1) / PS;
     const uint32_t lane = lane_id();
