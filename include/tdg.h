@@ -36,7 +36,8 @@
  * Status: 0 = ok, < 0 = error; tdg_last_error() returns a thread-local message.
  * Threading: a context owns one CUDA stream and its device buffers; calls on one
  * context are serialised by the caller; distinct contexts are independent (reentrant).
- * ctx == NULL selects a lazily created default context on the current device.
+ * ctx == NULL selects the calling thread's default context (created lazily on the thread's
+ * current device, destroyed at thread exit), so threads passing NULL never share buffers.
  * There is no CPU fallback: without a usable sm_100 device every compute call fails.
  */
 #ifndef TDG_H

@@ -424,9 +424,10 @@ cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uin
     const uint64_t slots = 2ull * m;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
     const size_t smem = 8u * kHSmall * sizeof(unsigned long long);
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(k_hbuild_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (attr != cudaSuccess) return attr;
+    // (a per-function attribute of the CURRENT device: set on every call, contexts may sit on
+    // different devices)
+    err = cudaFuncSetAttribute(k_hbuild_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (err != cudaSuccess) return err;
     k_hbuild_small<<<148u * 3u, 256, smem, st>>>(off, adj, eid, hoff4, n, htab);
     k_hinsert<<<gs, kThreads, 0, st>>>(off, adj, src, eid, hoff4, slots, htab);
     (*launches) += 2;

@@ -8,7 +8,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <cstdint>
-#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -280,8 +279,18 @@ struct tdg_context {
 
 namespace {
 
-std::mutex g_default_mu;
-tdg_context* g_default = nullptr;
+void destroy_ctx(tdg_context* ctx);
+
+// ctx == NULL: one default context per calling thread (created lazily on the thread's
+// current device, destroyed when the thread exits), so threads that pass NULL never share
+// device buffers or the pinned control block.
+struct DefaultCtx {
+    tdg_context* c = nullptr;
+    ~DefaultCtx() {
+        if (c) destroy_ctx(c);
+    }
+};
+thread_local DefaultCtx g_default;
 
 template <class F>
 int guarded(F&& f) {
@@ -325,15 +334,26 @@ void create_ctx(int device, tdg_context** out) {
     *out = c;
 }
 
+void destroy_ctx(tdg_context* ctx) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->trim();
+    for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    if (ctx->hctl) cudaFreeHost(ctx->hctl);
+    if (g_default.c == ctx) g_default.c = nullptr;
+    delete ctx;
+    cudaGetLastError();  // (at process exit the runtime may already be unloading)
+}
+
 tdg_context* resolve(tdg_context* ctx) {
     if (ctx) return ctx;
-    std::lock_guard<std::mutex> lk(g_default_mu);
-    if (!g_default) {
+    if (!g_default.c) {
         int dev = 0;
         cudaGetDevice(&dev);
-        create_ctx(dev, &g_default);
+        create_ctx(dev, &g_default.c);
     }
-    return g_default;
+    return g_default.c;
 }
 
 struct Dims {
@@ -406,6 +426,11 @@ void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, b
     ck(cudaEventRecord(c->ev[2], c->stream), "event");
 }
 
+void check_peel_ctl(const PeelCtl& pc) {
+    if (pc.nsl_overflow) throw Fail{TDG_ERR_RANGE, "sub-level trace overflow: a level index reached n+1"};
+    if (pc.chunk_overflow) throw Fail{TDG_ERR_RANGE, "internal error: compaction chunk table too small"};
+}
+
 void fill_times(tdg_times* t, tdg_context* c, bool host, bool peel) {
     if (!t) return;
     std::memset(t, 0, sizeof(*t));
@@ -462,8 +487,7 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         ck(cudaMemcpyAsync(&c->hctl->sup, c->sctl.p, sizeof(SupportCtl), cudaMemcpyDeviceToHost, c->stream), "D2H sctl");
         ck(cudaStreamSynchronize(c->stream), "decomposition");
         const PeelCtl& pc = c->hctl->peel;
-        if (pc.overflow || c->hctl->sup.overflow)
-            throw Fail{TDG_ERR_RANGE, "work queue exceeded 32-bit piece counter"};
+        check_peel_ctl(pc);
         const uint64_t len = d.m ? pc.levels_len : 0;
         if (const char* tp = std::getenv("TDG_TRACE")) {  // diagnostic dump: level, cs, W, ns, K
             const size_t k = std::min<size_t>(pc.sublevels, c->trace.cap / 32);
@@ -518,7 +542,6 @@ int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_
         ck(cudaEventRecord(c->ev[5], c->stream), "event");
         ck(cudaMemcpyAsync(&c->hctl->sup, c->sctl.p, sizeof(SupportCtl), cudaMemcpyDeviceToHost, c->stream), "D2H sctl");
         ck(cudaStreamSynchronize(c->stream), "support");
-        if (c->hctl->sup.overflow) throw Fail{TDG_ERR_RANGE, "work queue exceeded 32-bit piece counter"};
         fill_times(times, c, host, false);
     });
 }
@@ -539,18 +562,7 @@ int tdg_context_create(int device, tdg_context** out) {
 
 int tdg_context_destroy(tdg_context* ctx) {
     return guarded([&] {
-        if (!ctx) return;
-        cudaSetDevice(ctx->device);
-        cudaStreamSynchronize(ctx->stream);
-        ctx->trim();
-        for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
-        if (ctx->own) cudaStreamDestroy(ctx->own);
-        if (ctx->hctl) cudaFreeHost(ctx->hctl);
-        {
-            std::lock_guard<std::mutex> lk(g_default_mu);
-            if (g_default == ctx) g_default = nullptr;
-        }
-        delete ctx;
+        if (ctx) destroy_ctx(ctx);
     });
 }
 
@@ -901,7 +913,7 @@ int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32
         ck(cudaMemcpyAsync(in_next, c->f2.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H in_next");
         ck(cudaMemcpyAsync(&c->hctl->peel, pb.ctl, sizeof(PeelCtl), cudaMemcpyDeviceToHost, c->stream), "D2H ctl");
         ck(cudaStreamSynchronize(c->stream), "process_sublevel");
-        if (c->hctl->peel.overflow) throw Fail{TDG_ERR_RANGE, "work queue exceeded 32-bit piece counter"};
+        check_peel_ctl(c->hctl->peel);
         const uint32_t ns = c->hctl->peel.ph[1].out_size;
         if (ns) d2h(c->stream, next, pb.L[1], size_t(ns) * 4, "D2H next");
         *next_size = ns;

@@ -8,9 +8,10 @@
 // axis into equal pieces pulled dynamically by warps, so skew in list lengths never leaves
 // a warp with a long tail. Inside a piece a warp walks 32-item windows over consecutive
 // tasks: lane k holds task i+k and each lane finds its item's owner with a 5-step shuffle
-// search. Policy (per caller) supplies `load(t)`, `elems`, `find(task, x)` (edge id of the
-// searched side or kNone) and `visit(active, hit, task, ja, e)`, which all 32 lanes call together
-// (so it may use warp collectives).
+// search. Policy (per caller) supplies `load(t)`, `elems`, `kUnroll` (U items per lane per
+// step) and either `run<U>(act, task, ja)` (U > 1: the policy issues the U probe chains'
+// loads together) or, for U = 1, `find(task, x)` (edge id of the searched side or kNone) and
+// `visit(active, hit, task, ja, e)`; all 32 lanes call them together (warp collectives ok).
 #pragma once
 
 #include "tdg_common.cuh"
@@ -164,26 +165,7 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
             end_held = shfl64(s32, 31);
             held = i;
         }
-        unsigned long long limit = x1 < end_held ? x1 : end_held;
-        if (Policy::kHasStaged) {
-            // STAGED tasks (long, comparable lists) run alone over their in-piece range;
-            // the window below stops at the first staged task it holds.
-            const uint32_t smask = __ballot_sync(kFull, P.staged(k));
-            if (smask & 1u) {
-                const unsigned long long st0 = shfl64(st, 0), st1 = shfl64(st, 1);
-                const unsigned long long end0 = st1 < end_held ? st1 : end_held;
-                const unsigned long long lim0 = x1 < end0 ? x1 : end0;
-                P.staged_range(shfl_task(k, 0), static_cast<uint32_t>(base - st0),
-                               static_cast<uint32_t>(lim0 - st0));
-                if (lim0 == end0) i += 1;
-                base = lim0;
-                continue;
-            }
-            if (smask) {
-                const unsigned long long sm = shfl64(st, __ffs(smask) - 1);
-                limit = sm < limit ? sm : limit;
-            }
-        }
+        const unsigned long long limit = x1 < end_held ? x1 : end_held;
         const uint32_t relk = st <= base ? 0u
                               : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
         constexpr int U = Policy::kUnroll;

@@ -50,7 +50,6 @@ struct KcorePolicy {
     KcCtr* out;
     uint32_t* next;
     const uint32_t* elems;
-    static constexpr bool kHasStaged = false;
     static constexpr bool kFast = false;
     static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const {
@@ -64,8 +63,6 @@ struct KcorePolicy {
         k.aux = kNone;
         return k;
     }
-    __device__ bool staged(const ITask&) const { return false; }
-    __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
     __device__ uint32_t find(const ITask&, uint32_t w) const { return w; }
     __device__ void visit(bool active, bool, const ITask&, uint32_t, uint32_t w) const {
         bool app = false;

@@ -60,46 +60,27 @@ constexpr int kPeelThreads = TDG_PEEL_THREADS;
 constexpr int kScanItems = 8;
 constexpr int kWarps = kPeelThreads / 32;
 
-// Task of e1 = (u,v): probe the shorter live list a against the other endpoint b (id = e1,
-// aux = b, which never occurs in its own lists). Two forms:
-//  * HASH   (default): ob/lb = b's hash table (quad offset, slot mask);
-//  * STAGED (both lists long and of comparable length): ob = off[b], lb = dl[b] | kStaged;
-//    the piece's slice of N(b) is staged in shared memory and searched there (PeelPolicy).
-constexpr uint32_t kStaged = 0x80000000u;
+// Task of e1 = (u,v): probe the shorter live list a against the other endpoint b's
+// neighbour -> edge-id hash table (ob/lb = its quad offset and slot mask).
 #ifndef TDG_HTAB_NC
 #define TDG_HTAB_NC 0  // table slots through the read-only (non-coherent) path: tables never change in the peel
 #endif
 #ifndef TDG_PEEL_FAST
 #define TDG_PEEL_FAST 0  // engine fast path (intersect.cuh) for the peel's probe loop
 #endif
-#ifndef TDG_STAGE_MIN
-#define TDG_STAGE_MIN 0  // probe-list length from which a task may be staged (0 = off: measured faster with the filters)
-#endif
-#ifndef TDG_STAGE_RATIO
-#define TDG_STAGE_RATIO 8  // ... if the searched list is at most this many times longer
-#endif
-constexpr bool kDesc = TDG_STAGE_MIN == 0;  // task descriptors from prep (phase_prep)
-constexpr uint32_t kStageA = 128;  // probe elements per staged chunk
-constexpr uint32_t kStageB = 768;  // max searched-list slice held in shared memory (per warp)
 
 __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
     const uint2 p = g.el[e1];
     const uint32_t du = g.dl[p.x], dv = g.dl[p.y];
     const bool pu = du <= dv;
     const uint32_t a = pu ? p.x : p.y, b = pu ? p.y : p.x;
-    const uint32_t la = pu ? du : dv, lbl = pu ? dv : du;
     ITask k;
     k.id = e1;
     k.oa = g.off[a];
-    k.la = la;
+    k.la = pu ? du : dv;
     k.aux = b;
-    if (TDG_STAGE_MIN && la >= TDG_STAGE_MIN && static_cast<uint64_t>(lbl) <= static_cast<uint64_t>(la) * TDG_STAGE_RATIO) {
-        k.ob = g.off[b];
-        k.lb = lbl | kStaged;
-    } else {
-        k.ob = g.hoff4[b];
-        k.lb = 4u * (g.hoff4[b + 1] - k.ob) - 1u;
-    }
+    k.ob = g.hoff4[b];
+    k.lb = 4u * (g.hoff4[b + 1] - k.ob) - 1u;
     return k;
 }
 
@@ -128,34 +109,6 @@ __device__ __forceinline__ unsigned long long ld_state(const unsigned long long*
 }
 __device__ __forceinline__ uint32_t st_s(unsigned long long w) { return static_cast<uint32_t>(w); }
 __device__ __forceinline__ uint32_t st_stamp(unsigned long long w) { return static_cast<uint32_t>(w >> 32); }
-
-// try_decrement, truss_parallel.cpp:49-63, with the target's support `cur` already loaded.
-// Returns target if this thread moved it to the level (it then owns the append), else kNone;
-// `cross` = target if this decrement took it below the near bound B (a far edge entering
-// the near range, see phase_scan), else kNone.
-__device__ __forceinline__ uint32_t try_dec(unsigned long long* ss, uint32_t cur, uint32_t level, uint32_t K,
-                                            uint32_t B, uint32_t e1, uint32_t target, uint32_t other,
-                                            bool other_in_curr, uint32_t& cross) {
-    cross = kNone;
-    if (cur <= level) return kNone;                          // :52
-    if (other_in_curr && e1 >= other) return kNone;          // :53 ownership
-    const uint32_t prev = atomicSub(s_ptr(ss, target), 1u);  // :54
-    if (prev == level + 1) {                                 // :55-57
-        st_relaxed(stamp_ptr(ss, target), K + 1);
-        return target;
-    }
-    if (prev <= level) atomicAdd(s_ptr(ss, target), 1u);     // :58-62 repair
-    else if (prev == B) cross = target;
-    return kNone;
-}
-
-// Append up to two targets per lane to a list, one atomic per warp (appender.hpp:12-40).
-__device__ __forceinline__ void emit(uint32_t o0, uint32_t o1, uint32_t* ctr, uint32_t* list) {
-    const uint32_t p0 = warp_append(o0 != kNone, ctr);
-    if (o0 != kNone) list[p0] = o0;
-    const uint32_t p1 = warp_append(o1 != kNone, ctr);
-    if (o1 != kNone) list[p1] = o1;
-}
 
 // Append every lane's valid targets (o[j] != kNone) to next with one atomic per warp.
 template <int N>
@@ -191,23 +144,19 @@ struct PeelPolicy {
     uint32_t* next;
     const uint32_t* elems;
     unsigned long long* hit_ctr;  // diagnostic, may be null
-    uint32_t* stage;              // this warp's kStageB-entry shared buffer
     uint32_t B;                   // near bound (phase_scan): decrements from B append to X
     uint32_t* X;
     uint32_t* xcnt;
     const uint32_t* pbits;        // edges processed in earlier sub-levels (or null)
-    const uint4* desc;            // task descriptors written by phase_prep (or null)
-    static constexpr bool kHasStaged = TDG_STAGE_MIN != 0;
+    const uint4* desc;            // task descriptors written by phase_prep
     static constexpr bool kFast = TDG_PEEL_FAST;
     static constexpr int kUnroll = TDG_PEEL_U;
+    static_assert(kUnroll > 1, "the peel's probe loop is the U-chain form (run)");
     __device__ ITask load(uint32_t t) const {
-        if (kDesc && desc) {  // (aux = kNone: b's own id never occurs in its table, only a filter miss is lost)
-            const uint4 d = desc[t];
-            return ITask{curr[t], d.x, d.y, d.z, d.w, kNone};
-        }
-        return ptask(g, curr[t]);
+        // (aux = kNone: b's own id never occurs in its table, only a filter miss is lost)
+        const uint4 d = desc[t];
+        return ITask{curr[t], d.x, d.y, d.z, d.w, kNone};
     }
-    __device__ bool staged(const ITask& k) const { return (k.lb & kStaged) != 0; }
     // U hash-form probes per lane, stage by stage so the U chains' loads overlap:
     // list element + its edge id (coalesced) -> first table slot -> (collisions) ->
     // both peers' state words -> both decrements -> one warp append for all targets.
@@ -332,87 +281,6 @@ struct PeelPolicy {
                     if (hm) atomicAdd(hit_ctr, static_cast<unsigned long long>(__popc(hm)));
                     if (dm) atomicAdd(hit_ctr + 1, static_cast<unsigned long long>(__popc(dm)));
                 }
-            }
-        }
-    }
-    // A STAGED task's probe range [j0, j1): per kStageA-element chunk of N(a), the matching
-    // slice of N(b) (it starts where the previous one ended: both lists are sorted) is copied
-    // to shared memory with coalesced loads and searched there; a slice longer than kStageB
-    // (a locally skewed chunk) falls back to hash lookups.
-    __device__ void staged_range(const ITask& k, uint32_t j0, uint32_t j1) const {
-        const uint32_t lane = lane_id();
-        const uint32_t* A = g.adj + k.oa;
-        const uint32_t* B = g.adj + k.ob;
-        const uint32_t nbt = k.lb & ~kStaged, b = k.aux;
-        uint32_t lo = warp_bound_u32<false>(B, nbt, A[j0]);
-        for (uint32_t c0 = j0; c0 < j1; c0 += kStageA) {
-            const uint32_t c1 = min(j1, c0 + kStageA);
-            const uint32_t hi = lo + warp_bound_u32<true>(B + lo, nbt - lo, A[c1 - 1]);
-            const uint32_t nbr = hi - lo;
-            if (nbr <= kStageB) {
-                for (uint32_t q = lane; q < nbr; q += 32) stage[q] = B[lo + q];
-                __syncwarp();
-                for (uint32_t r = c0; r < c1; r += 32) {
-                    const uint32_t ja = r + lane;
-                    const bool active = ja < c1;
-                    uint32_t eb = kNone;
-                    if (active) {
-                        const uint32_t x = A[ja];
-                        const uint32_t pp = lower_bound_u32(stage, nbr, x);
-                        if (pp < nbr && stage[pp] == x) eb = g.eid[k.ob + lo + pp];
-                    }
-                    visit(active, eb != kNone, k, ja, eb);
-                }
-                __syncwarp();
-            } else {
-                const uint32_t q4 = g.hoff4[b];
-                const uint32_t mask = 4u * (g.hoff4[b + 1] - q4) - 1u;
-                for (uint32_t r = c0; r < c1; r += 32) {
-                    const uint32_t ja = r + lane;
-                    const bool active = ja < c1;
-                    uint32_t eb = kNone;
-                    if (active) {
-                        const uint32_t x = A[ja];
-                        if (x != b) {
-                            const uint32_t v = hlookup(g.htab + 4ull * q4, mask, x);
-                            eb = v == kNone ? kNone : (v & ~kHUp);
-                        }
-                    }
-                    visit(active, eb != kNone, k, ja, eb);
-                }
-            }
-            lo = hi;
-        }
-    }
-    __device__ uint32_t find(const ITask& k, uint32_t x) const {
-        if (x == k.aux) return kNone;
-        const uint32_t v = hlookup(g.htab + 4ull * k.ob, k.lb, x);
-        return v == kNone ? kNone : (v & ~kHUp);
-    }
-    __device__ void visit(bool active, bool hit, const ITask& k, uint32_t ja, uint32_t eb) const {
-        uint32_t o0 = kNone, o1 = kNone, c0 = kNone, c1 = kNone;
-        if (hit) {
-            const uint32_t ea = g.eid[k.oa + ja];
-            const unsigned long long wa = ld_state(ss, ea), wb = ld_state(ss, eb);
-            const uint32_t sa = st_stamp(wa), sb = st_stamp(wb);
-            if (!((sa != 0 && sa < K) || (sb != 0 && sb < K))) {                        // :85 processed peer
-                o0 = try_dec(ss, st_s(wa), level, K, B, k.id, ea, eb, sb == K, c0);  // :86
-                o1 = try_dec(ss, st_s(wb), level, K, B, k.id, eb, ea, sa == K, c1);  // :87
-            }
-        }
-        emit(o0, o1, &ph->out_size, next);
-        emit(c0, c1, xcnt, X);
-        if (hit_ctr) {  // diagnostics: hits, probes whose own slot is already processed
-            const uint32_t hm = __ballot_sync(kFull, hit);
-            bool dead = false;
-            if (active) {
-                const uint32_t sa = st_stamp(ld_state(ss, g.eid[k.oa + ja]));
-                dead = sa != 0 && sa < K;
-            }
-            const uint32_t dm = __ballot_sync(kFull, dead);
-            if (lane_id() == 0) {
-                if (hm) atomicAdd(hit_ctr, static_cast<unsigned long long>(__popc(hm)));
-                if (dm) atomicAdd(hit_ctr + 1, static_cast<unsigned long long>(__popc(dm)));
             }
         }
     }
@@ -590,18 +458,14 @@ __device__ void phase_bucket_scatter(const DevGraph& g, const uint32_t* curr, ui
 // Task descriptors: prep resolves each task's three levels of dependent random loads
 // (el -> dl -> off / table offset) once and stores {oa, la, ob, lb} in task order, so the
 // process phase's window refills are one coalesced 16-byte load per lane (the descriptor
-// loads were ~8 % of the peel's stall samples). Not used with staging (its tasks need aux).
+// loads were ~8 % of the peel's stall samples).
 
 __device__ void phase_prep(const DevGraph& g, const uint32_t* curr, uint32_t cs, unsigned long long* wpre,
                            unsigned long long* bsum, uint4* desc) {
     prep_items<kPeelThreads>(cs, [&](uint32_t t) {
-        if (kDesc && desc) {
-            const ITask k = ptask(g, curr[t]);
-            desc[t] = make_uint4(k.oa, k.la, k.ob, k.lb);
-            return k.la;
-        }
-        const uint2 p = g.el[curr[t]];
-        return min(g.dl[p.x], g.dl[p.y]);
+        const ITask k = ptask(g, curr[t]);
+        desc[t] = make_uint4(k.oa, k.la, k.ob, k.lb);
+        return k.la;
     }, wpre, bsum);
 }
 
@@ -625,8 +489,7 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             unsigned long long* hit_ctr, uint32_t B, uint32_t* X, uint32_t* xcnt,
                                             const uint32_t* pbits, const uint4* desc) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
-    __shared__ uint32_t sstage[TDG_STAGE_MIN ? kWarps * kStageB : 1];
-    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, sstage + (threadIdx.x >> 5) * kStageB, B, X, xcnt, pbits, desc};
+    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, B, X, xcnt, pbits, desc};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }
 
@@ -865,7 +728,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         // ---- sub-levels: prep + process (two grid barriers each; level 0 one)
         while (true) {
             if (leader) {
-                if (level < pb.nsl_cap) pb.nsl[level]++; else ctl->overflow = 1;
+                if (level < pb.nsl_cap) pb.nsl[level]++; else ctl->nsl_overflow = 1;
                 ctl->sublevels++;
                 ctl->levels_len = level + 1;
                 reset_ctr(&ctl->ph[(j + 1) % 3]);
@@ -935,7 +798,7 @@ __global__ void k_peel_init(const uint32_t* __restrict__ off, uint32_t n, uint32
             if (base + nc <= chunk_cap)
                 for (uint32_t k = 0; k < nc; k++) chunks[base + k] = make_uint2(u, k);
             else
-                ctl->overflow = 1;
+                ctl->chunk_overflow = 1;
         }
     }
     if (ss)  // pack the support pass result with stamp 0

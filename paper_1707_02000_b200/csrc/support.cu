@@ -88,12 +88,9 @@ struct SupportPolicy {
     const DevGraph& g;
     uint32_t* s;
     const uint32_t* elems;
-    static constexpr bool kHasStaged = false;
     static constexpr bool kFast = true;
     static constexpr int kUnroll = TDG_SUP_U;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
-    __device__ bool staged(const ITask&) const { return false; }
-    __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
     __device__ uint32_t find(const ITask& k, uint32_t x) const {
         const uint32_t p = lower_bound_u32(g.oadj + k.ob, k.lb, x);
         return (p < k.lb && g.oadj[k.ob + p] == x) ? p : kNone;
@@ -108,26 +105,6 @@ struct SupportPolicy {
 #pragma unroll
         for (int q = 0; q < U; q++) p[q] = act[q] ? find(ko[q], c[q]) : kNone;
         visit_all<U>(s, ko, ja, p);
-    }
-    // A hit closes triangle {x, y, c}: the oriented slots of y->c and x->c get one atomic
-    // each, the task's edge one per group of lanes sharing it (__match_any_sync).
-    __device__ void visit(bool, bool hit, const ITask& k, uint32_t ja, uint32_t p) const {
-        if (hit) {
-            atomicAdd(&s[k.oa + ja], 1u);
-            atomicAdd(&s[k.ob + p], 1u);
-        }
-        const uint32_t fm = __ballot_sync(kFull, hit);
-        if (fm) {
-            // usually every hitting lane works on the same task: one ballot instead of a match
-            const uint32_t first = __ffs(fm) - 1;
-            const uint32_t id0 = __shfl_sync(kFull, k.id, first);
-            if (__all_sync(kFull, !hit || k.id == id0)) {
-                if (lane_id() == first) atomicAdd(&s[id0], static_cast<uint32_t>(__popc(fm)));
-            } else if (hit) {
-                const uint32_t grp = __match_any_sync(fm, k.id);
-                if (lane_id() == static_cast<uint32_t>(__ffs(grp) - 1)) atomicAdd(&s[k.id], static_cast<uint32_t>(__popc(grp)));
-            }
-        }
     }
 };
 
@@ -170,12 +147,9 @@ struct SupportTabPolicy {
     const uint32_t* elems;
     const uint2* tab;
     uint32_t mask;
-    static constexpr bool kHasStaged = false;
     static constexpr bool kFast = true;
     static constexpr int kUnroll = TDG_SUP_U;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
-    __device__ bool staged(const ITask&) const { return false; }
-    __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
     __device__ uint32_t find(const ITask&, uint32_t c) const {
         uint32_t h = tab_hash(c, mask);
         while (true) {
@@ -195,9 +169,6 @@ struct SupportTabPolicy {
 #pragma unroll
         for (int q = 0; q < U; q++) p[q] = act[q] ? find(ko[q], c[q]) : kNone;
         visit_all<U>(s, ko, ja, p);
-    }
-    __device__ void visit(bool a, bool hit, const ITask& k, uint32_t ja, uint32_t p) const {
-        SupportPolicy{g, s, elems}.visit(a, hit, k, ja, p);
     }
 };
 
@@ -297,12 +268,9 @@ struct CountPolicy {
     const DevGraph& g;
     const uint32_t* elems;
     unsigned long long count = 0;
-    static constexpr bool kHasStaged = false;
     static constexpr bool kFast = true;
     static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
-    __device__ bool staged(const ITask&) const { return false; }
-    __device__ void staged_range(const ITask&, uint32_t, uint32_t) const {}
     __device__ uint32_t find(const ITask& k, uint32_t x) const {
         const uint32_t p = lower_bound_u32(g.oadj + k.ob, k.lb, x);
         return (p < k.lb && g.oadj[k.ob + p] == x) ? p : kNone;
@@ -370,9 +338,9 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* w
     }();
     if (tab_form) {
         const size_t smem = size_t(kSupTab) * sizeof(uint2);
-        static const cudaError_t attr =
-            cudaFuncSetAttribute(k_support_tab, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (attr != cudaSuccess) return attr;
+        // per-device attribute: set on every call (contexts may sit on different devices)
+        err = cudaFuncSetAttribute(k_support_tab, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (err != cudaSuccess) return err;
         int tb = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb, k_support_tab, kThreads, smem);
         if (tb < 1) tb = 1;

@@ -19,11 +19,6 @@ namespace tdg {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kNone = 0xffffffffu;
-// Load balancing: a task (edge) whose probe count exceeds kBigWork is split into
-// kPiece-item pieces served from a queue; smaller tasks are packed 32 per warp.
-constexpr uint32_t kBigWork = 256;
-constexpr uint32_t kPiece = 512;
-
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -111,18 +106,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
     return v;
 }
 
-// Owner lane of flat item `item` given per-lane exclusive prefixes `excl` (monotone):
-// the largest lane L with excl_L <= item. All 32 lanes must call.
-__device__ __forceinline__ uint32_t warp_owner(uint32_t excl, uint32_t item) {
-    uint32_t lo = 0;
-#pragma unroll
-    for (uint32_t step = 16; step > 0; step >>= 1) {
-        uint32_t e = __shfl_sync(kFull, excl, lo + step);
-        if (e <= item) lo += step;
-    }
-    return lo;
-}
-
 // Warp-aggregated append (the GPU form of BufferedAppender, appender.hpp:12-40): one
 // atomicAdd per warp. All 32 lanes must call; returns the slot for lanes with `pred`.
 __device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
@@ -133,28 +116,6 @@ __device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
     if (lane_id() == leader) base = atomicAdd(counter, static_cast<uint32_t>(__popc(mask)));
     base = __shfl_sync(kFull, base, leader);
     return base + static_cast<uint32_t>(__popc(mask & lanemask_lt()));
-}
-
-// Piece queue push: one packed 64-bit atomic returns (entry index, first piece) so the
-// entries' piece bases are ascending in entry order. Returns false on 32-bit overflow.
-__device__ __forceinline__ bool queue_push(unsigned long long* ctr, uint2* q, uint32_t task,
-                                           uint32_t work) {
-    uint32_t pieces = (work + kPiece - 1) / kPiece;
-    unsigned long long old = atomicAdd(ctr, (1ull << 32) | pieces);
-    uint32_t idx = static_cast<uint32_t>(old >> 32);
-    uint32_t base = static_cast<uint32_t>(old);
-    q[idx] = make_uint2(task, base);
-    return static_cast<unsigned long long>(base) + pieces <= 0xffffffffull;
-}
-
-// Entry owning piece p: last q with q[.].y <= p.
-__device__ __forceinline__ uint32_t queue_find(const uint2* q, uint32_t nq, uint32_t p) {
-    uint32_t lo = 0, hi = nq;  // invariant: q[lo].y <= p
-    while (hi - lo > 1) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (q[mid].y <= p) lo = mid; else hi = mid;
-    }
-    return lo;
 }
 
 // ---- per-vertex neighbour -> edge-id hash tables (built once per graph, never compacted)

@@ -65,7 +65,7 @@ cudaError_t launch_stats(const uint32_t* off, const uint32_t* eo, const uint32_t
 // ---- support (triangle.cpp:26-61 equivalent) ----
 struct SupportCtl {
     unsigned long long tri3; // sum of supports
-    uint32_t piece_head, overflow, smax, pad;
+    uint32_t piece_head, pad0, smax, pad;
     unsigned long long probes;  // probe items of the support pass
 };
 constexpr uint32_t kMaxChunks = 1024;  // max blocks of a prep grid (one work chunk each)
@@ -145,7 +145,8 @@ struct PeelCtl {
     uint32_t sublevels;
     uint32_t scans;
     uint32_t compactions;
-    uint32_t overflow;
+    uint32_t nsl_overflow;    // a level index reached the nsl capacity (n+1)
+    uint32_t chunk_overflow;  // the compaction chunk table was too small
     uint32_t final_stamp;
     uint32_t t_max;
     uint32_t nchunks;  // long-list compaction chunks (built by k_peel_init)

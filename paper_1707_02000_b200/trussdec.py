@@ -21,6 +21,7 @@ Arrays are numpy (uint32 per-edge, int64 offsets, int32 neighbours).
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -271,14 +272,16 @@ class Context:
                           d["deg_sum_dplus_sq"], d["deg_s1"])
 
 
-_default: Context | None = None
+_tls = threading.local()
 
 
 def default_context() -> Context:
-    global _default
-    if _default is None:
-        _default = Context(-1)
-    return _default
+    """Per-thread default context: ctypes releases the GIL during the C calls, so threads
+    sharing one context would race on its device buffers and pinned control block."""
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = _tls.ctx = Context(-1)
+    return ctx
 
 
 # ---------------------------------------------------------------- reference-named API
