@@ -84,7 +84,7 @@ typedef struct tdg_times {
     uint64_t scans;     /* scan passes actually executed (levels are skipped on device)   */
     uint64_t compactions; /* adjacency compactions executed inside the peel               */
     uint64_t probes;    /* peel probe items (hash lookups) over all sub-levels            */
-    uint64_t hits;      /* peel triangle visits (0 unless TDG_COUNT_HITS=1 in the env)    */
+    uint64_t hits;      /* peel triangle visits (0 unless TDG_COUNT=1 in the env)         */
     uint64_t dead_probes; /* probes of already-processed slots (same diagnostic switch)   */
     uint32_t t_max;     /* max trussness (0 when m == 0)                                  */
     uint32_t kernel_launches; /* kernels this call launched                               */
@@ -183,6 +183,37 @@ int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32
                          const uint32_t* curr, uint64_t curr_size, uint8_t* in_curr,
                          uint8_t* in_next, uint8_t* processed, uint32_t* next,
                          uint64_t* next_size);
+
+/* Access tallies of the context's last tdg_truss* / tdg_support* call, for byte models of
+ * the kernels (bench.py roofline). out[i] for i < min(cap, TDG_NCOUNTERS), in this order.
+ * The per-probe peel tallies (TDG_CNT_FILTER .. TDG_CNT_COMP_LONG) are counted only when
+ * the environment holds TDG_COUNT=1 at the call (a slower diagnostic instantiation of the
+ * peel kernel; the timed path never counts); the others are always counted. */
+enum {
+    TDG_CNT_FILTER = 0,     /* peel: membership-filter words read                          */
+    TDG_CNT_PBITS,          /* peel: processed-bitmap words read by probes                 */
+    TDG_CNT_WALK,           /* peel: hash-table walks (probes past filter + processed bit) */
+    TDG_CNT_SLOTS,          /* peel: hash-table slots read (first + collisions)            */
+    TDG_CNT_HITS,           /* peel: triangle visits (two edge-state words read)           */
+    TDG_CNT_DEAD,           /* peel: probes whose own slot was already processed           */
+    TDG_CNT_DEC,            /* peel: atomic decrements (truss_parallel.cpp:54)             */
+    TDG_CNT_REPAIR,         /* peel: repairs (truss_parallel.cpp:58-62)                    */
+    TDG_CNT_NEXT,           /* peel: next-frontier appends (truss_parallel.cpp:55-57)      */
+    TDG_CNT_CROSS,          /* peel: near/far crosser appends                              */
+    TDG_CNT_COMP_IN,        /* peel: adjacency-compaction entries read                     */
+    TDG_CNT_COMP_KEPT,      /* peel: compaction entries written back (short lists)         */
+    TDG_CNT_COMP_LONG,      /* peel: compaction entries kept in long lists (two copies)    */
+    TDG_CNT_SCAN_IN,        /* peel: scan entries read (live-list entry + edge state)      */
+    TDG_CNT_SCAN_OUT,       /* peel: scan entries written (curr / near / far lists)        */
+    TDG_CNT_TASKS,          /* peel: sub-level tasks (curr edges at levels > 0)            */
+    TDG_CNT_SORTED,         /* peel: tasks bucket-sorted by searched vertex                */
+    TDG_CNT_MARKS,          /* peel: processed-bitmap marks                                */
+    TDG_CNT_SUP_TAB_ELEMS,  /* support: N+(owner) elements loaded into shared-memory tables */
+    TDG_CNT_SUP_SEGMENTS,   /* support: owner segments served from a shared-memory table   */
+    TDG_CNT_SUP_SEARCH,     /* support: probe items binary-searched in global memory       */
+    TDG_NCOUNTERS
+};
+int tdg_counters(tdg_context* ctx, uint64_t* out, uint64_t cap);
 
 #ifdef __cplusplus
 }

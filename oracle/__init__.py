@@ -217,6 +217,10 @@ class Reference:
                                          C.POINTER(C.c_double)]
         L.ref_truss_parallel_kcore.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, C.c_int,
                                                C.POINTER(C.c_double)]
+        L.ref_prepare.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        L.ref_prepare.restype = C.c_void_p
+        L.ref_run.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_uint32)]
+        L.ref_free.argtypes = [C.c_void_p]
         L.ref_support_am4.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, C.c_int, _u32p]
         L.ref_build_truss_graph.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p, _u32p, _u32p]
         L.ref_truss_wc.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p]
@@ -255,6 +259,27 @@ class Reference:
         t = (C.c_double * 7)()
         self._check(self.lib.ref_truss_parallel_kcore(g.n, g.m, g.offsets, g.neighbors, workers, t))
         return dict(zip(("kcore", "reorder", "build", "support", "scan", "processing", "engine"), list(t)))
+
+    def prepare(self, g: Csr, workers: int, kcore: bool):
+        """Preprocess once (kcore -> coreness_order -> reorder if kcore) + build_truss_graph.
+        Returns (handle, {kcore, reorder, build} seconds); run with run(), release with free()."""
+        t = (C.c_double * 3)()
+        h = self.lib.ref_prepare(g.n, g.m, g.offsets, g.neighbors, workers, 1 if kcore else 0, t)
+        if not h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return h, dict(zip(("kcore", "reorder", "build"), list(t)))
+
+    def run(self, h, workers: int) -> dict:
+        """truss_parallel on a prepared graph: {support, scan, processing, engine, t_max}."""
+        t = (C.c_double * 4)()
+        tm = C.c_uint32()
+        self._check(self.lib.ref_run(h, workers, t, C.byref(tm)))
+        d = dict(zip(("support", "scan", "processing", "engine"), list(t)))
+        d["t_max"] = tm.value
+        return d
+
+    def free(self, h):
+        self.lib.ref_free(h)
 
     def support_am4(self, g: Csr, workers: int = 1) -> np.ndarray:
         s = np.zeros(max(g.m, 1), np.uint32)

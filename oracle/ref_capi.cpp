@@ -128,6 +128,52 @@ int ref_truss_parallel_kcore(int64_t n, int64_t m, const int64_t* off, const int
     });
 }
 
+// Prepared graph for repeated engine runs (bench.py --impl reference / cpu_baseline): the
+// reference's preprocessing runs once — with kcore != 0 its own pipeline kcore_parallel ->
+// coreness_order -> reorder (trussdec.cpp:92-97) — then build_truss_graph; ref_run times
+// truss_parallel alone, as the CLI's bench command does (trussdec.cpp:319-323).
+// prep_times: kcore, reorder, build (s). run times: support, scan, processing, engine (s).
+void* ref_prepare(int64_t n, int64_t m, const int64_t* off, const int32_t* nb, int workers, int kcore,
+                  double* prep_times) {
+    TrussGraph* out = nullptr;
+    guarded([&] {
+        CsrGraph g = to_csr(n, m, off, nb);
+        double t0 = now(), t1 = t0, t2 = t0;
+        if (kcore) {
+            CorenessResult cores = kcore_parallel(g, workers);
+            t1 = now();
+            g = reorder(g, coreness_order(cores));
+            t2 = now();
+        }
+        out = new TrussGraph(build_truss_graph(g));
+        const double t3 = now();
+        if (prep_times) {
+            prep_times[0] = t1 - t0;
+            prep_times[1] = t2 - t1;
+            prep_times[2] = t3 - t2;
+        }
+        return 0;
+    });
+    return out;
+}
+
+int ref_run(void* h, int workers, double* times, uint32_t* t_max) {
+    return guarded([&] {
+        const TrussGraph& tg = *static_cast<const TrussGraph*>(h);
+        const double t0 = now();
+        ParallelDecomposition dec = truss_parallel(tg, workers);
+        const double t1 = now();
+        times[0] = dec.times.support;
+        times[1] = dec.times.scan;
+        times[2] = dec.times.processing;
+        times[3] = t1 - t0;
+        if (t_max) *t_max = dec.result.t_max;
+        return 0;
+    });
+}
+
+void ref_free(void* h) { delete static_cast<TrussGraph*>(h); }
+
 int ref_support_am4(int64_t n, int64_t m, const int64_t* off, const int32_t* nb, int workers,
                     uint32_t* s_out) {
     return guarded([&] {

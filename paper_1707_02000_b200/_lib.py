@@ -75,6 +75,7 @@ SIGNATURES = [
     ("tdg_context_trim", _i32, [_vp]),
     ("tdg_truss", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp, _u64, _P(_u64), _P(tdg_times)]),
     ("tdg_truss_device", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp, _u64, _P(_u64), _P(tdg_times)]),
+    ("tdg_counters", _i32, [_vp, _P(_u64), _u64]),
     ("tdg_support", _i32, [_vp, _P(tdg_csr), _vp, _P(tdg_times)]),
     ("tdg_support_device", _i32, [_vp, _P(tdg_csr), _vp, _P(tdg_times)]),
     ("tdg_build_truss_graph", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp]),

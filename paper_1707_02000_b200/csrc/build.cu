@@ -115,22 +115,6 @@ __global__ void k_opos(const uint32_t* __restrict__ off, const uint32_t* __restr
     if (u <= n) opos[u] = pos[off[u]];
 }
 
-// Hash-table sizes in units of 4 slots: power of two >= max(4, 2d).
-__global__ void k_hsize(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ hq) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u < n) {
-        const uint32_t d = off[u + 1] - off[u];
-        uint32_t sz = 0;
-        if (d) {
-            sz = 4;
-            while (sz < 2 * d) sz <<= 1;
-        }
-        hq[u] = sz >> 2;
-    } else if (u == n) {
-        hq[n] = 0;
-    }
-}
-
 __device__ __forceinline__ unsigned long long htab_entry(const uint32_t* __restrict__ off, uint32_t x, uint32_t y,
                                                          uint32_t e) {
     const uint32_t dx = off[x + 1] - off[x], dy = off[y + 1] - off[y];
@@ -140,30 +124,32 @@ __device__ __forceinline__ unsigned long long htab_entry(const uint32_t* __restr
 
 // Tables of at most kHSmall slots are built in shared memory, one warp per vertex (up to kHMid,
 // one block per vertex), and written out with coalesced stores (random global CAS inserts were
-// 1.8 % of a C5 step).
+// 1.8 % of a C5 step). Table of x: kHF * d(x) slots at slot kHF * off[x] (tdg_common.cuh).
 constexpr uint32_t kHSmall = 1024;
 constexpr uint32_t kHMid = 8 * kHSmall;  // block-built tables use the block's whole 64 KB
 
+__device__ __forceinline__ void hinsert_smem(unsigned long long* t, uint32_t T, uint32_t y, unsigned long long entry) {
+    uint32_t h = hslot(hmix(y), T);
+    while (atomicCAS(&t[h], ~0ull, entry) != ~0ull) h = hnext(h, T);
+}
+
 __global__ void __launch_bounds__(256) k_hbuild_small(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                                      const uint32_t* __restrict__ eid, const uint32_t* __restrict__ hoff4,
-                                                      uint32_t n, unsigned long long* __restrict__ htab) {
+                                                      const uint32_t* __restrict__ eid, uint32_t n,
+                                                      unsigned long long* __restrict__ htab) {
     extern __shared__ unsigned long long htab_smem[];  // 8 warps x kHSmall slots
     const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     unsigned long long* t = htab_smem + w * kHSmall;
     for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < n; x += (gridDim.x * blockDim.x) >> 5) {
-        const uint32_t q0 = hoff4[x], T = 4u * (hoff4[x + 1] - q0);
+        const uint32_t o = off[x], d = off[x + 1] - o, T = kHF * d;
         if (T == 0 || T > kHSmall) continue;
         for (uint32_t i = lane; i < T; i += 32) t[i] = ~0ull;
         __syncwarp();
-        const uint32_t o = off[x], d = off[x + 1] - o;
         for (uint32_t i = lane; i < d; i += 32) {
             const uint32_t y = adj[o + i];
-            const unsigned long long entry = htab_entry(off, x, y, eid[o + i]);
-            uint32_t h = hmix(y) & (T - 1u);
-            while (atomicCAS(&t[h], ~0ull, entry) != ~0ull) h = (h + 1) & (T - 1u);
+            hinsert_smem(t, T, y, htab_entry(off, x, y, eid[o + i]));
         }
         __syncwarp();
-        unsigned long long* g = htab + 4ull * q0;
+        unsigned long long* g = htab + uint64_t(kHF) * o;
         for (uint32_t i = lane; i < T; i += 32) g[i] = t[i];
         __syncwarp();
     }
@@ -176,24 +162,21 @@ __global__ void __launch_bounds__(256) k_hbuild_small(const uint32_t* __restrict
         __syncthreads();
         const uint64_t x = c0 + threadIdx.x;
         if (x < n) {
-            const uint32_t T = 4u * (hoff4[x + 1] - hoff4[x]);
+            const uint32_t T = kHF * (off[x + 1] - off[x]);
             if (T > kHSmall && T <= kHMid) q[atomicAdd(&qn, 1u)] = static_cast<uint32_t>(x);
         }
         __syncthreads();
         const uint32_t cnt = qn;
         for (uint32_t k = 0; k < cnt; k++) {
-            const uint32_t v = q[k], q0 = hoff4[v], T = 4u * (hoff4[v + 1] - q0);
+            const uint32_t v = q[k], o = off[v], d = off[v + 1] - o, T = kHF * d;
             for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) htab_smem[i] = ~0ull;
             __syncthreads();
-            const uint32_t o = off[v], d = off[v + 1] - o;
             for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
                 const uint32_t y = adj[o + i];
-                const unsigned long long entry = htab_entry(off, v, y, eid[o + i]);
-                uint32_t h = hmix(y) & (T - 1u);
-                while (atomicCAS(&htab_smem[h], ~0ull, entry) != ~0ull) h = (h + 1) & (T - 1u);
+                hinsert_smem(htab_smem, T, y, htab_entry(off, v, y, eid[o + i]));
             }
             __syncthreads();
-            unsigned long long* g = htab + 4ull * q0;
+            unsigned long long* g = htab + uint64_t(kHF) * o;
             for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) g[i] = htab_smem[i];
             __syncthreads();
         }
@@ -203,31 +186,29 @@ __global__ void __launch_bounds__(256) k_hbuild_small(const uint32_t* __restrict
 // Insert every slot (x -> y, eid) of a big table into x's table; the value carries the
 // orientation bit.
 __global__ void k_hinsert(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                          const uint32_t* __restrict__ src, const uint32_t* __restrict__ eid,
-                          const uint32_t* __restrict__ hoff4, uint64_t slots, unsigned long long* __restrict__ htab) {
+                          const uint32_t* __restrict__ src, const uint32_t* __restrict__ eid, uint64_t slots,
+                          unsigned long long* __restrict__ htab) {
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t x = src[j], y = adj[j];
-        if (4u * (hoff4[x + 1] - hoff4[x]) <= kHMid) continue;
-        const uint32_t dx = off[x + 1] - off[x], dy = off[y + 1] - off[y];
-        const bool up = dx < dy || (dx == dy && x < y);
-        const unsigned long long entry = (static_cast<unsigned long long>(eid[j] | (up ? kHUp : 0u)) << 32) | y;
-        unsigned long long* tab = htab + 4ull * hoff4[x];
-        const uint32_t mask = 4u * (hoff4[x + 1] - hoff4[x]) - 1u;
-        uint32_t h = hmix(y) & mask;
-        while (atomicCAS(&tab[h], ~0ull, entry) != ~0ull) h = (h + 1) & mask;
+        const uint32_t o = off[x], T = kHF * (off[x + 1] - o);
+        if (T <= kHMid) continue;
+        unsigned long long* tab = htab + uint64_t(kHF) * o;
+        const unsigned long long entry = htab_entry(off, x, y, eid[j]);
+        uint32_t h = hslot(hmix(y), T);
+        while (atomicCAS(&tab[h], ~0ull, entry) != ~0ull) h = hnext(h, T);
     }
 }
 
 // Filter bits of every slot (x -> y) whose owner table is big enough (tdg_common.cuh).
-__global__ void k_finsert(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ src,
-                          const uint32_t* __restrict__ hoff4, uint64_t slots, unsigned long long* __restrict__ filt) {
+__global__ void k_finsert(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                          const uint32_t* __restrict__ src, uint64_t slots, unsigned long long* __restrict__ filt) {
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t x = src[j], y = adj[j];
-        const uint32_t q0 = hoff4[x], T = 4u * (hoff4[x + 1] - q0);
-        if (T < kFMin) continue;
-        atomicOr(&filt[(q0 >> kFShift) + (fword(y) & ((T >> (kFShift + 2)) - 1u))], fbits(hmix(y)));
+        const uint32_t o = off[x], d = off[x + 1] - o;
+        if (kHF * d < kFMin) continue;
+        atomicOr(&filt[fword_index(o, d, y)], fbits(hmix(y)));
     }
 }
 
@@ -332,8 +313,8 @@ size_t build_cub_bytes(uint32_t n, uint32_t m) {
     cub::DeviceScan::ExclusiveSum(nullptr, c, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
                                   slots + 1);
     size_t d = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, d, static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-                                    static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), m > 0 ? m : 1);
+    cub::DoubleBuffer<uint32_t> keys(nullptr, nullptr), vals(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, d, keys, vals, m > 0 ? m : 1);
     c = c > d ? c : d;
     size_t r = a > b ? a : b;
     return r > c ? r : c;
@@ -364,9 +345,11 @@ cudaError_t launch_build(const BuildBufs& b, uint32_t n, uint32_t m, bool with_o
     int bits = 1;
     while (bits < 32 && (1ull << bits) < n) bits++;
     tmp = b.cub_bytes;
-    err = cub::DeviceRadixSort::SortPairs(b.cub_tmp, tmp, b.oadj, b.osrc, b.oeid, b.stask, m, 0, bits, st);
+    // double-buffered (no m-sized temporaries): the sorted ids end in either value buffer
+    cub::DoubleBuffer<uint32_t> keys(b.oadj, b.osrc), vals(b.oeid, b.stask);
+    err = cub::DeviceRadixSort::SortPairs(b.cub_tmp, tmp, keys, vals, m, 0, bits, st);
     if (err != cudaSuccess) return err;
-    k_eid_lower<<<gs, kThreads, 0, st>>>(b.adj, b.src, b.P, b.stask, slots, b.eid);
+    k_eid_lower<<<gs, kThreads, 0, st>>>(b.adj, b.src, b.P, vals.Current(), slots, b.eid);
     (*launches) += 2;
     if (!with_orientation) return cudaGetLastError();
     if ((err = cudaMemsetAsync(b.flag + slots, 0, sizeof(uint32_t), st)) != cudaSuccess) return err;
@@ -407,41 +390,32 @@ cudaError_t launch_to_ref(const uint32_t* oeid, const uint32_t* in, uint32_t m, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_htab_sizes(const uint32_t* off, uint32_t n, uint32_t* hq, uint32_t* hoff4, void* cub_tmp,
-                              size_t cub_bytes, cudaStream_t st, uint32_t* launches) {
-    k_hsize<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(off, n, hq);
-    (*launches)++;
-    size_t tmp = cub_bytes;
-    return cub::DeviceScan::ExclusiveSum(cub_tmp, tmp, hq, hoff4, static_cast<uint64_t>(n) + 1, st);
-}
-
 cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, const uint32_t* eid,
-                             const uint32_t* hoff4, uint32_t n, uint32_t m, unsigned long long* htab, uint64_t htab_slots,
-                             cudaStream_t st, uint32_t* launches) {
+                             uint32_t n, uint32_t m, unsigned long long* htab, cudaStream_t st, uint32_t* launches) {
     if (m == 0) return cudaSuccess;
-    cudaError_t err = cudaMemsetAsync(htab, 0xff, htab_slots * sizeof(unsigned long long), st);
-    if (err != cudaSuccess) return err;
     const uint64_t slots = 2ull * m;
+    cudaError_t err = cudaMemsetAsync(htab, 0xff, htab_slots(m) * sizeof(unsigned long long), st);
+    if (err != cudaSuccess) return err;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
     const size_t smem = 8u * kHSmall * sizeof(unsigned long long);
     // (a per-function attribute of the CURRENT device: set on every call, contexts may sit on
     // different devices)
     err = cudaFuncSetAttribute(k_hbuild_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (err != cudaSuccess) return err;
-    k_hbuild_small<<<148u * 3u, 256, smem, st>>>(off, adj, eid, hoff4, n, htab);
-    k_hinsert<<<gs, kThreads, 0, st>>>(off, adj, src, eid, hoff4, slots, htab);
+    k_hbuild_small<<<148u * 3u, 256, smem, st>>>(off, adj, eid, n, htab);
+    k_hinsert<<<gs, kThreads, 0, st>>>(off, adj, src, eid, slots, htab);
     (*launches) += 2;
     return cudaGetLastError();
 }
 
-cudaError_t launch_filter_fill(const uint32_t* adj, const uint32_t* src, const uint32_t* hoff4, uint32_t m,
-                               unsigned long long* filt, uint64_t filt_words, cudaStream_t st, uint32_t* launches) {
+cudaError_t launch_filter_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, uint32_t m,
+                               unsigned long long* filt, cudaStream_t st, uint32_t* launches) {
     if (m == 0) return cudaSuccess;
-    cudaError_t err = cudaMemsetAsync(filt, 0, filt_words * sizeof(unsigned long long), st);
+    cudaError_t err = cudaMemsetAsync(filt, 0, filter_words(m) * sizeof(unsigned long long), st);
     if (err != cudaSuccess) return err;
     const uint64_t slots = 2ull * m;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
-    k_finsert<<<gs, kThreads, 0, st>>>(adj, src, hoff4, slots, filt);
+    k_finsert<<<gs, kThreads, 0, st>>>(off, adj, src, slots, filt);
     (*launches)++;
     return cudaGetLastError();
 }

@@ -72,7 +72,7 @@ struct HostCtl {
     PeelCtl peel;
     SupportCtl sup;
     StatsAcc stats;
-    uint32_t htab_quads;
+    uint32_t word;  // small D2H scalar (component count, c_max, reorder check)
 };
 
 }  // namespace
@@ -86,38 +86,70 @@ struct tdg_context {
     int sms = 148;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
-    DevBuf off64, off, adj, src, eo, up, P, eid, el, flag, pos, opos, oadj, oeid, osrc, stask, sx, sbeg;
-    DevBuf cchunk, cscr, pbits;
-    DevBuf dl, s, stamp, L0, L1, A0, A1, F0, F1, X0, X1, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, hoff4, htab, filt, Ls, bhist, bcur, trace;
+    // persistent per-graph arrays (live through the peel)
+    DevBuf off64, off, adj, eo, up, P, eid, el, opos, oeid, sbeg, dl, pbits, htab, filt;
+    // one arena for the m-sized scratch: the build + support arrays and the peel lists share
+    // it (they are never live at the same time; layout in ensure_arena)
+    DevBuf arena;
+    DevBuf cchunk, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, bhist, bcur, trace;
     DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing;
+    // arena views (recomputed by ensure_arena)
+    uint32_t *src = nullptr, *flag = nullptr, *pos = nullptr, *oadj = nullptr, *osrc = nullptr, *stask = nullptr,
+             *sx = nullptr, *s = nullptr, *L0 = nullptr, *L1 = nullptr, *Ls = nullptr, *A0 = nullptr, *A1 = nullptr,
+             *F0 = nullptr, *F1 = nullptr, *X0 = nullptr, *X1 = nullptr, *cscr = nullptr;
+    unsigned long long *ss = nullptr, *wpre = nullptr;
+    size_t word = 0;
     HostCtl* hctl = nullptr;
     cudaEvent_t ev[8] = {};
     uint32_t launches = 0;
 
     void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
 
+    // Arena of 17 "words" of 4(m+1) bytes (256-aligned). Build + support use words
+    //   2-3 src (-> support work prefix wpre), 4-5 flag (-> internal-id scratch), 6-7 pos,
+    //   8 oadj, 9 osrc, 10 stask, 11 sx, 16 s,
+    // the peel uses 0-1 ss (packed state), 2-3 wpre, 4-7 cscr (task descriptors /
+    // compaction scratch), 8 L0, 9 L1, 10 Ls, 11 A0, 12 A1, 13 F0, 14 F1, 15 X0, 16 X1.
+    // s (16) is read by k_peel_init while it writes ss (0-1); X1 (16) is first written by
+    // the peel's crosser appends, after that.
+    static constexpr int kArenaWords = 17;
+    static size_t arena_word(uint64_t m) { return (4 * (m + 1) + 255) & ~size_t(255); }
+    void ensure_arena(uint64_t m) {
+        word = arena_word(m);
+        arena.ensure(kArenaWords * word, "arena (build / support / peel scratch)");
+        char* b = arena.as<char>();
+        auto w32 = [&](int i) { return reinterpret_cast<uint32_t*>(b + i * word); };
+        ss = reinterpret_cast<unsigned long long*>(b);
+        wpre = reinterpret_cast<unsigned long long*>(b + 2 * word);
+        src = w32(2);
+        cscr = flag = w32(4);
+        pos = w32(6);
+        L0 = oadj = w32(8);
+        L1 = osrc = w32(9);
+        Ls = stask = w32(10);
+        A0 = sx = w32(11);
+        A1 = w32(12);
+        F0 = w32(13);
+        F1 = w32(14);
+        X0 = w32(15);
+        X1 = s = w32(16);
+    }
+
     void ensure_graph(uint64_t n, uint64_t m) {
         const uint64_t slots = 2 * m;
         off64.ensure((n + 1) * 8, "offsets64");
         off.ensure((n + 1) * 4, "offsets");
         adj.ensure(slots * 4, "adj");
-        src.ensure(slots * 4, "src");
         eo.ensure(n * 4, "eo");
         up.ensure((n + 1) * 4, "up");
         P.ensure((n + 1) * 4, "P");
         eid.ensure(slots * 4, "eid");
         el.ensure(m * 8, "el");
-        flag.ensure((slots + 1) * 4, "flag");
-        pos.ensure((slots + 1) * 4, "pos");
         opos.ensure((n + 1) * 4, "opos");
-        oadj.ensure(m * 4, "oadj");
         oeid.ensure(m * 4, "oeid");
-        osrc.ensure(m * 4, "osrc");
-        stask.ensure(m * 4, "stask");
-        sx.ensure(m * 4, "sx");
         sbeg.ensure((n + 1) * 4, "sbeg");
         dl.ensure(n * 4, "dl");
-        s.ensure(m * 4, "support");
+        ensure_arena(m);
         ctl.ensure(sizeof(PeelCtl), "ctl");
         sctl.ensure(sizeof(SupportCtl), "sctl");
         sacc.ensure(sizeof(StatsAcc), "stats");
@@ -125,25 +157,14 @@ struct tdg_context {
         bsum.ensure(sizeof(unsigned long long) * kMaxChunks, "bsum");
     }
     void ensure_peel(uint64_t n, uint64_t m) {
-        stamp.ensure(m * 8, "edge state");
-        L0.ensure(m * 4, "L0");
-        L1.ensure(m * 4, "L1");
-        A0.ensure(m * 4, "A0");
-        A1.ensure(m * 4, "A1");
-        F0.ensure(m * 4, "F0");
-        F1.ensure(m * 4, "F1");
-        X0.ensure(m * 4, "X0");
-        X1.ensure(m * 4, "X1");
-        Ls.ensure(m * 4, "Ls");
+        ensure_arena(m);
         if (bhist.cap == 0) {
             bhist.ensure(kBuckets * 4, "bhist");
             ck(cudaMemsetAsync(bhist.p, 0, kBuckets * 4, stream), "memset");
         }
         bcur.ensure(kBuckets * 4, "bcur");
         nsl.ensure((n + 2) * 4, "nsl");
-        const uint64_t cc = chunk_cap(m);
-        cchunk.ensure(cc * 12, "compaction chunks");
-        cscr.ensure(m * 16, "compaction scratch");
+        cchunk.ensure(chunk_cap(m) * 12, "compaction chunks");
         pbits.ensure((m + 31) / 32 * 4, "processed bitmap");
     }
     static uint64_t chunk_cap(uint64_t m) { return (2 * m) / 512 + (2 * m) / 2048 + 2; }
@@ -153,20 +174,20 @@ struct tdg_context {
         b.off64 = off64_dev;
         b.off = off.as<uint32_t>();
         b.adj = adj.as<uint32_t>();
-        b.src = src.as<uint32_t>();
+        b.src = src;
         b.eo = eo.as<uint32_t>();
         b.up = up.as<uint32_t>();
         b.P = P.as<uint32_t>();
         b.eid = eid.as<uint32_t>();
         b.el = el.as<uint2>();
-        b.flag = flag.as<uint32_t>();
-        b.pos = pos.as<uint32_t>();
+        b.flag = flag;
+        b.pos = pos;
         b.opos = opos.as<uint32_t>();
-        b.oadj = oadj.as<uint32_t>();
+        b.oadj = oadj;
         b.oeid = oeid.as<uint32_t>();
-        b.osrc = osrc.as<uint32_t>();
-        b.stask = stask.as<uint32_t>();
-        b.sx = sx.as<uint32_t>();
+        b.osrc = osrc;
+        b.stask = stask;
+        b.sx = sx;
         b.sbeg = sbeg.as<uint32_t>();
         b.cub_tmp = cub.p;
         b.cub_bytes = cub.cap;
@@ -182,37 +203,36 @@ struct tdg_context {
         g.el = el.as<uint2>();
         g.dl = dl.as<uint32_t>();
         g.opos = opos.as<uint32_t>();
-        g.oadj = oadj.as<uint32_t>();
+        g.oadj = oadj;
         g.oeid = oeid.as<uint32_t>();
-        g.osrc = osrc.as<uint32_t>();
-        g.stask = stask.as<uint32_t>();
-        g.sx = sx.as<uint32_t>();
+        g.osrc = osrc;
+        g.stask = stask;
+        g.sx = sx;
         g.sbeg = sbeg.as<uint32_t>();
-        g.hoff4 = hoff4.as<uint32_t>();
         g.htab = htab.as<unsigned long long>();
         g.filt = peel_filter() ? filt.as<unsigned long long>() : nullptr;
         return g;
     }
     PeelBufs peel_bufs(uint32_t n) const {
         PeelBufs p;
-        p.s = s.as<uint32_t>();
-        p.ss = stamp.as<unsigned long long>();
-        p.L[0] = L0.as<uint32_t>();
-        p.L[1] = L1.as<uint32_t>();
-        p.A[0] = A0.as<uint32_t>();
-        p.A[1] = A1.as<uint32_t>();
-        p.F[0] = F0.as<uint32_t>();
-        p.F[1] = F1.as<uint32_t>();
-        p.X[0] = X0.as<uint32_t>();
-        p.X[1] = X1.as<uint32_t>();
-        p.wpre = src.as<unsigned long long>();  // build scratch (2m u32), free once built
+        p.s = s;
+        p.ss = ss;
+        p.L[0] = L0;
+        p.L[1] = L1;
+        p.A[0] = A0;
+        p.A[1] = A1;
+        p.F[0] = F0;
+        p.F[1] = F1;
+        p.X[0] = X0;
+        p.X[1] = X1;
+        p.wpre = wpre;
         p.bsum = bsum.as<unsigned long long>();
         p.ctl = ctl.as<PeelCtl>();
         p.nsl = nsl.as<uint32_t>();
         p.nsl_cap = n + 1;
-        const char* ch = std::getenv("TDG_COUNT_HITS");
-        p.count_hits = (ch && ch[0] == '1') ? 1u : 0u;
-        p.Ls = Ls.as<uint32_t>();
+        const char* ch = std::getenv("TDG_COUNT");
+        p.count = (ch && ch[0] == '1') ? 1u : 0u;
+        p.Ls = Ls;
         p.bhist = bhist.as<uint32_t>();
         p.bcur = bcur.as<uint32_t>();
         uint32_t bits = 0;
@@ -228,20 +248,21 @@ struct tdg_context {
         p.chunk_cap = static_cast<uint32_t>(cc);
         p.chunks = cchunk.as<uint2>();
         p.ckept = reinterpret_cast<uint32_t*>(p.chunks + cc);
-        p.sadj = cscr.as<uint32_t>();
-        p.seid = p.sadj ? p.sadj + cscr.cap / 8 : nullptr;
-        // sub-level task descriptors share the compaction scratch (m x 16 B): compaction runs
-        // only between a scan and the first sub-level of a level
-        p.desc = cscr.as<uint4>();
+        // compaction scratch: 2 x 2m u32 in words 4-7; the sub-level task descriptors (16 B per
+        // curr edge) share it — compaction runs only between a scan and the first sub-level
+        p.sadj = cscr;
+        p.seid = cscr + word / 2;  // 2 words later (word is in bytes: 2 * word / 4 u32)
+        p.desc = reinterpret_cast<uint4*>(cscr);
         p.pbits = pbits.as<uint32_t>();
         return p;
     }
     void trim() {
-        DevBuf* all[] = {&off64, &off, &adj, &src, &eo, &up, &P, &eid, &el, &flag, &pos, &opos, &oadj, &oeid,
-                         &osrc, &stask, &sx, &sbeg, &dl, &s, &stamp, &L0, &L1, &A0, &A1, &F0, &F1, &X0, &X1, &nsl, &ctl, &sctl, &sacc, &cub,
-                         &truss, &sup, &f0, &f1, &f2, &bsum, &hoff4, &htab, &filt, &Ls, &bhist, &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1,
-                         &kwpre, &kctl, &ktmp, &knoff, &knadj, &kperm, &kbad, &ing, &cchunk, &cscr, &pbits};
+        DevBuf* all[] = {&off64, &off, &adj, &eo, &up, &P, &eid, &el, &opos, &oeid, &sbeg, &dl, &pbits, &htab, &filt,
+                         &arena, &cchunk, &nsl, &ctl, &sctl, &sacc, &cub, &truss, &sup, &f0, &f1, &f2, &bsum, &bhist,
+                         &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1, &kwpre, &kctl, &ktmp, &knoff, &knadj,
+                         &kperm, &kbad, &ing};
         for (DevBuf* b : all) b->release();
+        word = 0;
     }
     KcoreBufs kcore_bufs(uint64_t n, uint64_t m) {
         kdeg.ensure((n + 2) * 4, "kdeg");
@@ -331,6 +352,7 @@ void create_ctx(int device, tdg_context** out) {
     c->stream = c->own;
     for (auto& ev : c->ev) ck(cudaEventCreate(&ev), "cudaEventCreate");
     ck(cudaMallocHost(reinterpret_cast<void**>(&c->hctl), sizeof(HostCtl)), "cudaMallocHost");
+    std::memset(c->hctl, 0, sizeof(HostCtl));
     *out = c;
 }
 
@@ -401,26 +423,16 @@ void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, b
     ck(cudaEventRecord(c->ev[1], c->stream), "event");
     ck(launch_build(c->build_bufs(off64), d.n, d.m, orient, c->stream, &c->launches), "build kernels");
     if (internal)  // flag (2m+1 u32) is free once the build is done
-        ck(launch_internal_ids(c->build_bufs(off64), d.m, c->flag.as<uint32_t>(), c->stream, &c->launches),
+        ck(launch_internal_ids(c->build_bufs(off64), d.m, c->flag, c->stream, &c->launches),
            "internal edge ids");
-    if (tables) {
-        // neighbour -> edge-id hash tables; their total size is read back once to size htab
-        c->hoff4.ensure((size_t(d.n) + 1) * 4, "hoff4");
-        ck(launch_htab_sizes(c->off.as<uint32_t>(), d.n, c->up.as<uint32_t>(), c->hoff4.as<uint32_t>(), c->cub.p,
-                             c->cub.cap, c->stream, &c->launches), "hash sizes");
-        ck(cudaMemcpyAsync(&c->hctl->htab_quads, c->hoff4.as<uint32_t>() + d.n, 4, cudaMemcpyDeviceToHost, c->stream),
-           "D2H table size");
-        ck(cudaStreamSynchronize(c->stream), "table size");
-        const uint64_t slots = 4ull * c->hctl->htab_quads;
-        c->htab.ensure(slots * 8, "hash tables");
-        ck(launch_htab_fill(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->src.as<uint32_t>(), c->eid.as<uint32_t>(),
-                            c->hoff4.as<uint32_t>(), d.n, d.m, c->htab.as<unsigned long long>(), slots, c->stream,
-                            &c->launches), "hash fill");
+    if (tables) {  // neighbour -> edge-id hash tables (+ filters): sizes depend on m only
+        c->htab.ensure(htab_slots(d.m) * 8, "hash tables");
+        ck(launch_htab_fill(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->src, c->eid.as<uint32_t>(), d.n, d.m,
+                            c->htab.as<unsigned long long>(), c->stream, &c->launches), "hash fill");
         if (peel_filter()) {
-            const uint64_t words = (c->hctl->htab_quads >> kFShift) + 1;
-            c->filt.ensure(words * 8, "filters");
-            ck(launch_filter_fill(c->adj.as<uint32_t>(), c->src.as<uint32_t>(), c->hoff4.as<uint32_t>(), d.m,
-                                  c->filt.as<unsigned long long>(), words, c->stream, &c->launches), "filter fill");
+            c->filt.ensure(filter_words(d.m) * 8, "filters");
+            ck(launch_filter_fill(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->src, d.m,
+                                  c->filt.as<unsigned long long>(), c->stream, &c->launches), "filter fill");
         }
     }
     ck(cudaEventRecord(c->ev[2], c->stream), "event");
@@ -462,13 +474,13 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
         c->ensure_peel(d.n, d.m);
         if (std::getenv("TDG_TRACE")) c->trace.ensure(size_t(32) << 20, "trace");
         const DevGraph dg = c->dev_graph(d.n, d.m);
-        ck(launch_support(dg, c->s.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
+        ck(launch_support(dg, c->s, c->wpre, c->bsum.as<unsigned long long>(),
                           c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
         uint32_t* sup_dev = nullptr;
         if (support_out && d.m) {
             if (host) { c->sup.ensure(size_t(d.m) * 4, "support copy"); sup_dev = c->sup.as<uint32_t>(); }
             else sup_dev = support_out;
-            ck(launch_to_ref(dg.oeid, c->s.as<uint32_t>(), d.m, 0, sup_dev, c->stream, &c->launches), "support copy");
+            ck(launch_to_ref(dg.oeid, c->s, d.m, 0, sup_dev, c->stream, &c->launches), "support copy");
         }
         ck(cudaEventRecord(c->ev[3], c->stream), "event");
         const PeelBufs pb = c->peel_bufs(d.n);
@@ -515,8 +527,8 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
             times->process_ms = pc.proc_ns * 1e-6;
             times->compact_ms = pc.compact_ns * 1e-6;
             times->probes = pc.probes;
-            times->hits = pc.hits;
-            times->dead_probes = pc.dead;
+            times->hits = pc.cnt[kCntHits];
+            times->dead_probes = pc.cnt[kCntDead];
             times->t_max = d.m ? pc.t_max : 0;
         }
     });
@@ -533,9 +545,9 @@ int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_
         const DevGraph dg = c->dev_graph(d.n, d.m);
         uint32_t* sdev = support_out;
         if (host) { c->sup.ensure(size_t(d.m) * 4 + 4, "support copy"); sdev = c->sup.as<uint32_t>(); }
-        ck(launch_support(dg, c->s.as<uint32_t>(), c->src.as<unsigned long long>(), c->bsum.as<unsigned long long>(),
+        ck(launch_support(dg, c->s, c->wpre, c->bsum.as<unsigned long long>(),
                           c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
-        ck(launch_to_ref(dg.oeid, c->s.as<uint32_t>(), d.m, 0, sdev, c->stream, &c->launches), "support to ref ids");
+        ck(launch_to_ref(dg.oeid, c->s, d.m, 0, sdev, c->stream, &c->launches), "support to ref ids");
         ck(cudaEventRecord(c->ev[3], c->stream), "event");
         if (host && d.m)
             ck(cudaMemcpyAsync(support_out, sdev, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H support");
@@ -631,7 +643,7 @@ int tdg_triangle_count(tdg_context* ctx, const tdg_csr* g, uint64_t* count, tdg_
         const Dims d = check_graph(g, true);
         c->launches = 0;
         stage_and_build(c, g, d, true, true, false);
-        ck(launch_triangle_count(c->dev_graph(d.n, d.m), c->src.as<unsigned long long>(),
+        ck(launch_triangle_count(c->dev_graph(d.n, d.m), c->wpre,
                                  c->bsum.as<unsigned long long>(), c->sctl.as<SupportCtl>(), c->sms, c->stream,
                                  &c->launches), "triangle count");
         ck(cudaEventRecord(c->ev[3], c->stream), "event");
@@ -669,18 +681,18 @@ int tdg_ktruss_components(tdg_context* ctx, const tdg_csr* g, const uint32_t* tr
         KtrussBufs kb;
         kb.parent = c->dl.as<uint32_t>();
         kb.first = c->up.as<uint32_t>();
-        kb.root_of_edge = c->L0.as<uint32_t>();
+        kb.root_of_edge = c->L0;
         kb.flag = c->f0.as<uint32_t>();
         kb.rank = c->f1.as<uint32_t>();
-        kb.comp = c->L1.as<uint32_t>();
+        kb.comp = c->L1;
         kb.cub_tmp = c->cub.p;
         kb.cub_bytes = c->cub.cap;
         ck(launch_ktruss(c->el.as<uint2>(), c->truss.as<uint32_t>(), d.n, d.m, k, kb, c->stream, &c->launches),
            "ktruss kernels");
         ck(cudaMemcpyAsync(comp_of_edge, kb.comp, size_t(d.m) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H comp");
-        ck(cudaMemcpyAsync(&c->hctl->htab_quads, kb.rank + d.m, 4, cudaMemcpyDeviceToHost, c->stream), "D2H ncomp");
+        ck(cudaMemcpyAsync(&c->hctl->word, kb.rank + d.m, 4, cudaMemcpyDeviceToHost, c->stream), "D2H ncomp");
         ck(cudaStreamSynchronize(c->stream), "ktruss");
-        *ncomp = c->hctl->htab_quads;
+        *ncomp = c->hctl->word;
     });
 }
 
@@ -698,10 +710,10 @@ int tdg_kcore(tdg_context* ctx, const tdg_csr* g, uint32_t* core_out, uint32_t* 
                         kb.deg + d.n), "kcore kernel");
         if (d.n) {
             ck(cudaMemcpyAsync(core_out, kb.core, size_t(d.n) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H core");
-            ck(cudaMemcpyAsync(&c->hctl->htab_quads, kb.deg + d.n, 4, cudaMemcpyDeviceToHost, c->stream), "D2H c_max");
+            ck(cudaMemcpyAsync(&c->hctl->word, kb.deg + d.n, 4, cudaMemcpyDeviceToHost, c->stream), "D2H c_max");
         }
         ck(cudaStreamSynchronize(c->stream), "kcore");
-        *c_max = d.n ? c->hctl->htab_quads : 0;
+        *c_max = d.n ? c->hctl->word : 0;
     });
 }
 
@@ -743,9 +755,9 @@ int tdg_reorder(tdg_context* ctx, const tdg_csr* g, const uint32_t* perm, int64_
         ck(launch_reorder(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->kperm.as<uint32_t>(), d.n, d.m, kb,
                           c->knoff.as<uint32_t>(), c->knadj.as<uint32_t>(), c->kbad.as<uint32_t>(), c->stream,
                           &c->launches), "reorder");
-        ck(cudaMemcpyAsync(&c->hctl->htab_quads, c->kbad.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H check");
+        ck(cudaMemcpyAsync(&c->hctl->word, c->kbad.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H check");
         ck(cudaStreamSynchronize(c->stream), "reorder");
-        if (c->hctl->htab_quads)  // graph.cpp:106-113
+        if (c->hctl->word)  // graph.cpp:106-113
             throw Fail{TDG_ERR_INVALID, "reorder: permutation is not a bijection on 0..n-1"};
         std::vector<uint32_t> noff(size_t(d.n) + 1);
         d2h(c->stream, noff.data(), c->knoff.p, noff.size() * 4, "D2H offsets");
@@ -854,14 +866,12 @@ int tdg_scan(tdg_context* ctx, const uint32_t* s, uint64_t m, uint32_t level, co
         *curr_size = 0;
         if (m == 0) return;
         const uint32_t mm = static_cast<uint32_t>(m);
-        c->s.ensure(m * 4, "support");
         c->ensure_peel(0, m);
         c->ctl.ensure(sizeof(PeelCtl), "ctl");
-        c->src.ensure(m * 8, "wpre");
         c->bsum.ensure(sizeof(unsigned long long) * kMaxChunks, "bsum");
         c->f0.ensure(m, "processed");
         c->f1.ensure(m, "in_curr");
-        ck(cudaMemcpyAsync(c->s.p, s, m * 4, cudaMemcpyHostToDevice, c->stream), "H2D s");
+        ck(cudaMemcpyAsync(c->s, s, m * 4, cudaMemcpyHostToDevice, c->stream), "H2D s");
         ck(cudaMemcpyAsync(c->f0.p, processed, m, cudaMemcpyHostToDevice, c->stream), "H2D processed");
         ck(cudaMemcpyAsync(c->f1.p, in_curr, m, cudaMemcpyHostToDevice, c->stream), "H2D in_curr");
         ck(cudaMemsetAsync(c->ctl.p, 0, sizeof(PeelCtl), c->stream), "memset");
@@ -897,17 +907,17 @@ int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32
         c->f1.ensure(d.m, "in_curr");
         c->f2.ensure(d.m, "in_next");
         const size_t m = d.m;
-        ck(cudaMemcpyAsync(c->s.p, s, m * 4, cudaMemcpyHostToDevice, c->stream), "H2D s");
+        ck(cudaMemcpyAsync(c->s, s, m * 4, cudaMemcpyHostToDevice, c->stream), "H2D s");
         ck(cudaMemcpyAsync(c->f0.p, processed, m, cudaMemcpyHostToDevice, c->stream), "H2D processed");
         ck(cudaMemcpyAsync(c->f1.p, in_curr, m, cudaMemcpyHostToDevice, c->stream), "H2D in_curr");
         ck(cudaMemcpyAsync(c->f2.p, in_next, m, cudaMemcpyHostToDevice, c->stream), "H2D in_next");
-        if (curr_size) ck(cudaMemcpyAsync(c->L0.p, curr, curr_size * 4, cudaMemcpyHostToDevice, c->stream), "H2D curr");
+        if (curr_size) ck(cudaMemcpyAsync(c->L0, curr, curr_size * 4, cudaMemcpyHostToDevice, c->stream), "H2D curr");
         ck(cudaMemsetAsync(c->ctl.p, 0, sizeof(PeelCtl), c->stream), "memset");
         const DevGraph dg = c->dev_graph(d.n, d.m);
         const PeelBufs pb = c->peel_bufs(d.n);
         ck(launch_step_process(dg, pb, level, static_cast<uint32_t>(curr_size), c->f1.as<uint8_t>(),
                                c->f2.as<uint8_t>(), c->f0.as<uint8_t>(), c->sms, c->stream), "process_sublevel");
-        ck(cudaMemcpyAsync(s, c->s.p, m * 4, cudaMemcpyDeviceToHost, c->stream), "D2H s");
+        ck(cudaMemcpyAsync(s, c->s, m * 4, cudaMemcpyDeviceToHost, c->stream), "D2H s");
         ck(cudaMemcpyAsync(processed, c->f0.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H processed");
         ck(cudaMemcpyAsync(in_curr, c->f1.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H in_curr");
         ck(cudaMemcpyAsync(in_next, c->f2.p, m, cudaMemcpyDeviceToHost, c->stream), "D2H in_next");
@@ -917,6 +927,23 @@ int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32
         const uint32_t ns = c->hctl->peel.ph[1].out_size;
         if (ns) d2h(c->stream, next, pb.L[1], size_t(ns) * 4, "D2H next");
         *next_size = ns;
+    });
+}
+
+static_assert(int(TDG_CNT_SCAN_IN) == int(kCntScanIn) && int(TDG_CNT_MARKS) == int(kCntMarks) &&
+                  int(TDG_CNT_COMP_LONG) == int(kCntCompLong) && int(TDG_CNT_SUP_TAB_ELEMS) == int(kPeelCnt),
+              "tdg.h counter order must follow PeelCnt");
+
+int tdg_counters(tdg_context* ctx, uint64_t* out, uint64_t cap) {
+    return guarded([&] {
+        if (!out && cap) throw Fail{TDG_ERR_INVALID, "out is NULL"};
+        tdg_context* c = resolve(ctx);
+        uint64_t v[TDG_NCOUNTERS];
+        for (int i = 0; i < kPeelCnt; i++) v[i] = c->hctl->peel.cnt[i];
+        v[TDG_CNT_SUP_TAB_ELEMS] = c->hctl->sup.tab_elems;
+        v[TDG_CNT_SUP_SEGMENTS] = c->hctl->sup.tab_segments;
+        v[TDG_CNT_SUP_SEARCH] = c->hctl->sup.search_items;
+        for (uint64_t i = 0; i < cap && i < TDG_NCOUNTERS; i++) out[i] = v[i];
     });
 }
 

@@ -61,7 +61,8 @@ constexpr int kScanItems = 8;
 constexpr int kWarps = kPeelThreads / 32;
 
 // Task of e1 = (u,v): probe the shorter live list a against the other endpoint b's
-// neighbour -> edge-id hash table (ob/lb = its quad offset and slot mask).
+// neighbour -> edge-id hash table (ob = off[b], lb = d(b): the table is kHF * d(b) slots at
+// slot kHF * off[b], tdg_common.cuh).
 #ifndef TDG_HTAB_NC
 #define TDG_HTAB_NC 0  // table slots through the read-only (non-coherent) path: tables never change in the peel
 #endif
@@ -79,8 +80,8 @@ __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
     k.oa = g.off[a];
     k.la = pu ? du : dv;
     k.aux = b;
-    k.ob = g.hoff4[b];
-    k.lb = 4u * (g.hoff4[b + 1] - k.ob) - 1u;
+    k.ob = g.off[b];
+    k.lb = g.off[b + 1] - k.ob;
     return k;
 }
 
@@ -134,7 +135,10 @@ __device__ __forceinline__ void emit_many(const uint32_t (&o)[N], uint32_t* ctr,
 
 // process_sublevel's inner loop (truss_parallel.cpp:80-88) as a probe-engine policy: a hit
 // is w in N(u) ∩ N(v): slot ja of the probe list (its eid is one peer) found in the other
-// endpoint's hash table (whose value is the other peer's id).
+// endpoint's hash table (whose value is the other peer's id). kCount = the diagnostic
+// instantiation that also tallies every access class of the probe (PeelCnt, for the byte
+// model of bench.py); the timed path is the kCount = false instantiation.
+template <bool kCount>
 struct PeelPolicy {
     const DevGraph& g;
     unsigned long long* ss;
@@ -143,7 +147,7 @@ struct PeelPolicy {
     PhaseCtr* ph;
     uint32_t* next;
     const uint32_t* elems;
-    unsigned long long* hit_ctr;  // diagnostic, may be null
+    unsigned long long* cnt;      // PeelCnt counters (kCount only)
     uint32_t B;                   // near bound (phase_scan): decrements from B append to X
     uint32_t* X;
     uint32_t* xcnt;
@@ -164,6 +168,7 @@ struct PeelPolicy {
     __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
         uint32_t x[U], ea[U], eb[U], h[U];
         unsigned long long ent[U];
+        uint32_t cn[kCntProbe] = {};  // per-lane access tallies (kCount only; folded away otherwise)
 #pragma unroll
         for (int q = 0; q < U; q++) {
             x[q] = kHEmpty;
@@ -184,14 +189,19 @@ struct PeelPolicy {
         // bit (L2-resident bitmap, consecutive lanes share words) is read beside the filter
         uint32_t pw[U];
 #pragma unroll
-        for (int q = 0; q < U; q++) pw[q] = (pbits && look[q]) ? pbits[ea[q] >> 5] : 0u;
+        for (int q = 0; q < U; q++) {
+            pw[q] = (pbits && look[q]) ? pbits[ea[q] >> 5] : 0u;
+            if constexpr (kCount) cn[kCntPbits] += (pbits && look[q]) ? 1u : 0u;
+        }
         if (g.filt) {
             unsigned long long fw[U];
 #pragma unroll
             for (int q = 0; q < U; q++) {
                 fw[q] = ~0ull;
-                if (look[q] && ko[q].lb + 1u >= kFMin)
-                    fw[q] = __ldg(g.filt + (ko[q].ob >> kFShift) + (fword(x[q]) & (((ko[q].lb + 1u) >> (kFShift + 2)) - 1u)));
+                if (look[q] && kHF * ko[q].lb >= kFMin) {
+                    fw[q] = __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q]));
+                    if constexpr (kCount) cn[kCntFilter]++;
+                }
             }
 #pragma unroll
             for (int q = 0; q < U; q++) {
@@ -202,12 +212,15 @@ struct PeelPolicy {
 #pragma unroll
         for (int q = 0; q < U; q++)
             if ((pw[q] >> (ea[q] & 31u)) & 1u) look[q] = false;
+        const unsigned long long* tb[U];  // b's table: kHF * d(b) slots at slot kHF * off[b]
 #pragma unroll
         for (int q = 0; q < U; q++) {
             ent[q] = kHEmpty;
+            tb[q] = g.htab + uint64_t(kHF) * ko[q].ob;
             if (look[q]) {
-                h[q] &= ko[q].lb;
-                ent[q] = TDG_HTAB_NC ? __ldg(g.htab + 4ull * ko[q].ob + h[q]) : g.htab[4ull * ko[q].ob + h[q]];
+                h[q] = hslot(h[q], kHF * ko[q].lb);
+                ent[q] = TDG_HTAB_NC ? __ldg(tb[q] + h[q]) : tb[q][h[q]];
+                if constexpr (kCount) { cn[kCntWalk]++; cn[kCntSlots]++; }
             }
         }
 #pragma unroll
@@ -215,8 +228,9 @@ struct PeelPolicy {
             unsigned long long e = ent[q];
             uint32_t hh = h[q];
             while (static_cast<uint32_t>(e) != kHEmpty && static_cast<uint32_t>(e) != x[q]) {
-                hh = (hh + 1) & ko[q].lb;
-                e = TDG_HTAB_NC ? __ldg(g.htab + 4ull * ko[q].ob + hh) : g.htab[4ull * ko[q].ob + hh];
+                hh = hnext(hh, kHF * ko[q].lb);
+                e = TDG_HTAB_NC ? __ldg(tb[q] + hh) : tb[q][hh];
+                if constexpr (kCount) cn[kCntSlots]++;
             }
             eb[q] = (x[q] != kHEmpty && static_cast<uint32_t>(e) == x[q]) ? (static_cast<uint32_t>(e >> 32) & ~kHUp)
                                                                            : kNone;
@@ -229,6 +243,7 @@ struct PeelPolicy {
             if (eb[q] != kNone) {
                 wa[q] = ld_state(ss, ea[q]);
                 wb[q] = ld_state(ss, eb[q]);
+                if constexpr (kCount) cn[kCntHits]++;
             }
         }
         // try_dec (truss_parallel.cpp:49-63) split so all atomics issue before any result is used
@@ -255,32 +270,34 @@ struct PeelPolicy {
             o[j] = kNone;
             c[j] = kNone;
             if (tg[j] != kNone) {
+                if constexpr (kCount) cn[kCntDec]++;
                 if (pv[j] == level + 1) {  // :55-57
                     st_relaxed(stamp_ptr(ss, tg[j]), K + 1);
                     o[j] = tg[j];
+                    if constexpr (kCount) cn[kCntNext]++;
                 } else if (pv[j] <= level) {
                     atomicAdd(s_ptr(ss, tg[j]), 1u);  // :58-62 repair
+                    if constexpr (kCount) cn[kCntRepair]++;
                 } else if (pv[j] == B) {
                     c[j] = tg[j];  // crossed below the near bound
+                    if constexpr (kCount) cn[kCntCross]++;
                 }
             }
         }
         emit_many(o, &ph->out_size, next);
         emit_many(c, xcnt, X);
-        if (hit_ctr) {
+        if constexpr (kCount) {
 #pragma unroll
             for (int q = 0; q < U; q++) {
-                const uint32_t hm = __ballot_sync(kFull, eb[q] != kNone);
-                bool dead = false;
                 if (act[q]) {
                     const uint32_t sa = st_stamp(ld_state(ss, ea[q]));
-                    dead = sa != 0 && sa < K;
+                    cn[kCntDead] += (sa != 0 && sa < K) ? 1u : 0u;
                 }
-                const uint32_t dm = __ballot_sync(kFull, dead);
-                if (lane_id() == 0) {
-                    if (hm) atomicAdd(hit_ctr, static_cast<unsigned long long>(__popc(hm)));
-                    if (dm) atomicAdd(hit_ctr + 1, static_cast<unsigned long long>(__popc(dm)));
-                }
+            }
+#pragma unroll
+            for (int k = 0; k < kCntProbe; k++) {
+                const uint32_t t = __reduce_add_sync(kFull, cn[k]);
+                if (lane_id() == 0 && t) atomicAdd(cnt + k, static_cast<unsigned long long>(t));
             }
         }
     }
@@ -482,14 +499,15 @@ __device__ __forceinline__ bool processed_bit(const uint32_t* pbits, uint32_t e)
 }
 
 // process_sublevel (truss_parallel.cpp:39-104) for curr[0..cs) on the intersection engine.
+template <bool kCount>
 __device__ unsigned long long phase_process(const DevGraph& g, unsigned long long* ss, uint32_t level,
                                             uint32_t K, const uint32_t* curr, uint32_t cs,
                                             const unsigned long long* wpre, const unsigned long long* bsum,
                                             uint32_t nchunks, PhaseCtr* ph, uint32_t* next,
-                                            unsigned long long* hit_ctr, uint32_t B, uint32_t* X, uint32_t* xcnt,
+                                            unsigned long long* cnt, uint32_t B, uint32_t* X, uint32_t* xcnt,
                                             const uint32_t* pbits, const uint4* desc) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
-    PeelPolicy P{g, ss, level, K, curr, ph, next, g.adj, hit_ctr, B, X, xcnt, pbits, desc};
+    PeelPolicy<kCount> P{g, ss, level, K, curr, ph, next, g.adj, cnt, B, X, xcnt, pbits, desc};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }
 
@@ -517,8 +535,8 @@ constexpr int kCompactU = 4;  // entries per lane per compaction round
 
 __device__ __forceinline__ bool long_list(const DevGraph& g, uint32_t u) { return g.off[u + 1] - g.off[u] > kBigList; }
 
-__device__ void phase_compact_long(const DevGraph& g, unsigned long long* ss, uint32_t K, const PeelBufs& pb,
-                                   uint32_t nchunks) {
+template <bool kCount>
+__device__ void phase_compact_long(const DevGraph& g, const PeelBufs& pb, uint32_t nchunks) {
     const uint32_t lane = lane_id();
     const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
     for (uint32_t c = gw; c < nchunks; c += nw) {
@@ -555,7 +573,13 @@ __device__ void phase_compact_long(const DevGraph& g, unsigned long long* ss, ui
                 }
             }
         }
-        if (lane == 0) pb.ckept[c] = kept;
+        if (lane == 0) {
+            pb.ckept[c] = kept;
+            if constexpr (kCount) {
+                if (lo < dlu) atomicAdd(&pb.ctl->cnt[kCntCompIn], static_cast<unsigned long long>(min(dlu, lo + kChunk) - lo));
+                atomicAdd(&pb.ctl->cnt[kCntCompLong], static_cast<unsigned long long>(kept));
+            }
+        }
     }
 }
 
@@ -587,7 +611,8 @@ __device__ void phase_compact_copy(const DevGraph& g, const PeelBufs& pb, uint32
 // keeps kCompactU state loads in flight. Writes stay in list order: an entry's new slot is
 // its list's kept count before this round (per-vertex counter in shared memory) plus the
 // kept entries before it in the round.
-__device__ void phase_compact_short(const DevGraph& g, const uint32_t* pbits) {
+template <bool kCount>
+__device__ void phase_compact_short(const DevGraph& g, const uint32_t* pbits, unsigned long long* cnt) {
     __shared__ uint32_t sh_kept[kWarps][32];
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
@@ -647,6 +672,13 @@ __device__ void phase_compact_short(const DevGraph& g, const uint32_t* pbits) {
             }
         }
         if (len) g.dl[u] = sh_kept[wid][lane];
+        if constexpr (kCount) {
+            const uint32_t kept = __reduce_add_sync(kFull, len ? sh_kept[wid][lane] : 0u);
+            if (lane == 0) {
+                atomicAdd(cnt + kCntCompIn, static_cast<unsigned long long>(total));
+                atomicAdd(cnt + kCntCompKept, static_cast<unsigned long long>(kept));
+            }
+        }
         __syncwarp();
     }
 }
@@ -660,6 +692,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
 
 // The whole truss_parallel level loop (truss_parallel.cpp:119-144) in one launch.
+template <bool kCount>
 __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g, PeelBufs pb) {
     cg::grid_group grid = cg::this_grid();
     PeelCtl* ctl = pb.ctl;
@@ -680,6 +713,8 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         if (leader) {
             reset_ctr(&ctl->ph[(j + 1) % 3]);
             ctl->scans++;
+            ctl->cnt[kCntScanIn] += static_cast<unsigned long long>(in.nA) + in.nX + in.nF;
+            ctl->cnt[kCntMarks] += pend_n;
             ctl->xcnt[xp ^ 1] = 0;  // crossers after this scan (read by the previous scan)
             if (resplit) ctl->rebuilds++;
         }
@@ -703,6 +738,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             fi ^= 1;
             nF = vload(&r->far_size);
         }
+        if (leader) ctl->cnt[kCntScanOut] += static_cast<unsigned long long>(cs) + nA + (resplit ? nF : 0u);
         if (cs == 0) {
             if (nA == 0) {
                 if (nF == 0) break;
@@ -716,8 +752,8 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         const unsigned long long live = static_cast<unsigned long long>(cs) + nA + nF;
         if (level > 0 && live * kCompactDen < static_cast<unsigned long long>(live_at_compact) * kCompactNum) {
             if (leader) { reset_ctr(&ctl->ph[(j + 1) % 3]); ctl->compactions++; }
-            phase_compact_long(g, pb.ss, K, pb, nchunks);
-            phase_compact_short(g, pb.pbits);
+            phase_compact_long<kCount>(g, pb, nchunks);
+            phase_compact_short<kCount>(g, pb.pbits, ctl->cnt);
             grid.sync();
             phase_compact_copy(g, pb, nchunks);
             grid.sync();
@@ -730,6 +766,11 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             if (leader) {
                 if (level < pb.nsl_cap) pb.nsl[level]++; else ctl->nsl_overflow = 1;
                 ctl->sublevels++;
+                ctl->cnt[kCntMarks] += pend_n;
+                if (level > 0) {
+                    ctl->cnt[kCntTasks] += cs;
+                    if (kSortMin && cs >= kSortMin) ctl->cnt[kCntSorted] += cs;
+                }
                 ctl->levels_len = level + 1;
                 reset_ctr(&ctl->ph[(j + 1) % 3]);
             }
@@ -750,9 +791,9 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                 phase_prep(g, tasks, cs, pb.wpre, pb.bsum, pb.desc);
                 grid.sync();
                 const unsigned long long W =
-                    phase_process(g, pb.ss, level, K, tasks, cs, pb.wpre, pb.bsum, gridDim.x,
-                                  &ctl->ph[j % 3], pb.L[li ^ 1], pb.count_hits ? &ctl->hits : nullptr, B,
-                                  pb.X[xp], &ctl->xcnt[xp], pb.pbits, pb.desc);
+                    phase_process<kCount>(g, pb.ss, level, K, tasks, cs, pb.wpre, pb.bsum, gridDim.x,
+                                          &ctl->ph[j % 3], pb.L[li ^ 1], ctl->cnt, B, pb.X[xp], &ctl->xcnt[xp],
+                                          pb.pbits, pb.desc);
                 if (leader) {
                     ctl->probes += W;
                     sub_w = W;
@@ -848,8 +889,8 @@ __global__ void __launch_bounds__(kPeelThreads) k_step_prep(DevGraph g, PeelBufs
 // Hand-built states may break the level-0 invariant, so the step form always probes.
 __global__ void __launch_bounds__(kPeelThreads) k_step_process(DevGraph g, PeelBufs pb, uint32_t cs, uint32_t level,
                                                                uint32_t nchunks) {
-    phase_process(g, pb.ss, level, 2, pb.L[0], cs, pb.wpre, pb.bsum, nchunks, &pb.ctl->ph[1], pb.L[1],
-                  nullptr, 0xffffffffu, nullptr, &pb.ctl->xcnt[0], nullptr, pb.desc);
+    phase_process<false>(g, pb.ss, level, 2, pb.L[0], cs, pb.wpre, pb.bsum, nchunks, &pb.ctl->ph[1], pb.L[1],
+                         nullptr, 0xffffffffu, nullptr, &pb.ctl->xcnt[0], nullptr, pb.desc);
 }
 
 // Epilogue (truss_parallel.cpp:97-102) + in_next flags for the appended edges; unpacks s.
@@ -876,8 +917,10 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     if (g.m == 0) return cudaSuccess;
     if (p.pbits && (err = cudaMemsetAsync(p.pbits, 0, size_t((g.m + 31) / 32) * 4, st)) != cudaSuccess) return err;
     k_peel_init<<<148 * 4, 256, 0, st>>>(g.off, g.n, g.dl, p.s, g.m, p.ss, p.ctl, p.chunks, p.chunk_cap);
+    // count mode (diagnostic, PeelBufs::count): the instantiation that tallies every access
+    const void* kern = p.count ? reinterpret_cast<const void*>(k_peel<true>) : reinterpret_cast<const void*>(k_peel<false>);
     int per_sm = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_peel, kPeelThreads, 0);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPeelThreads, 0);
     if (err != cudaSuccess) return err;
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
     unsigned blocks = static_cast<unsigned>(sm_count * per_sm);
@@ -885,7 +928,7 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     DevGraph gg = g;
     PeelBufs pp = p;
     void* args[] = {&gg, &pp};
-    err = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_peel), dim3(blocks), dim3(kPeelThreads), args, 0, st);
+    err = cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(kPeelThreads), args, 0, st);
     (*launches) += 2;
     return err;
 }

@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
                 j = tend;
             }
             if (bend > base) {
+                if (threadIdx.x == 0) atomicAdd(&ctl->search_items, bend - base);
                 const unsigned long long w0 = base + (bend - base) * wid / kSupWarps;
                 const unsigned long long w1 = base + (bend - base) * (wid + 1) / kSupWarps;
                 if (w0 < w1) run_items(SP, w0, w1, task_in(w0, i, j, wpre, sboff, CH), m, wpre, sboff, CH);
@@ -235,6 +236,10 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
             uint32_t size = 64;
             while (size < TDG_SUP_LOAD * dp && size < kSupTab) size <<= 1;  // load <= 1/LOAD, or <= 3/4 at full size
             for (uint32_t q = threadIdx.x; q < size; q += kThreads) tab[q] = make_uint2(kHEmpty, 0u);
+            if (threadIdx.x == 0) {
+                atomicAdd(&ctl->tab_elems, static_cast<unsigned long long>(dp));
+                atomicAdd(&ctl->tab_segments, 1ull);
+            }
             __syncthreads();
             const uint32_t o = g.opos[x];
             for (uint32_t q = threadIdx.x; q < dp; q += kThreads) {

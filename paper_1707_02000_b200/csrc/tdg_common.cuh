@@ -119,9 +119,15 @@ __device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
 }
 
 // ---- per-vertex neighbour -> edge-id hash tables (built once per graph, never compacted)
-// Table of x: htab[4*hoff4[x] .. 4*hoff4[x+1]), power-of-two size >= max(4, 2*d(x)),
-// linear probing. Entry = (value << 32) | key, key = neighbour id (kHEmpty = free slot),
+// Table of x: kHF * d(x) slots at slot offset kHF * off[x] (load factor exactly 1/kHF; the
+// layout is a pure function of the CSR offsets, so the total kHF * 2m is known before the
+// build — no size readback). Linear probing from slot hslot(hmix(key), T), wrapping at T.
+// Entry = (value << 32) | key, key = neighbour id (kHEmpty = free slot),
 // value = edge id | (neighbour after x in the (degree, id) order ? 1<<31 : 0).
+#ifndef TDG_HT_FACTOR
+#define TDG_HT_FACTOR 2  // table slots per neighbour (C5: 2 -> 32 B per edge of tables)
+#endif
+constexpr uint32_t kHF = TDG_HT_FACTOR;
 constexpr uint32_t kHEmpty = 0xffffffffu;
 constexpr uint32_t kHUp = 0x80000000u;
 
@@ -133,36 +139,28 @@ __device__ __forceinline__ uint32_t hmix(uint32_t x) {
     x ^= x >> 16;
     return x;
 }
-
-// Value stored for `key` in the table at `tab` (mask = size-1), or kNone.
-__device__ __forceinline__ uint32_t hlookup(const unsigned long long* __restrict__ tab, uint32_t mask, uint32_t key) {
-    uint32_t h = hmix(key) & mask;
-    while (true) {
-        const unsigned long long e = tab[h];
-        const uint32_t k = static_cast<uint32_t>(e);
-        if (k == key) return static_cast<uint32_t>(e >> 32);
-        if (k == kHEmpty) return kNone;
-        h = (h + 1) & mask;
-    }
-}
+// First slot of hash h in a table of T slots (multiply-high range reduction, any T).
+__device__ __forceinline__ uint32_t hslot(uint32_t h, uint32_t T) { return __umulhi(h, T); }
+__device__ __forceinline__ uint32_t hnext(uint32_t i, uint32_t T) { return i + 1 == T ? 0u : i + 1; }
 
 // ---- per-vertex membership filters (register-blocked Bloom filters) in front of the big
-// tables. A table of T >= kFMin slots owns T/2^(kFShift+2) 64-bit words at word offset
-// hoff4 >> kFShift (big tables have quad counts divisible by 2^kFShift, so regions never
-// overlap) — >= 32/2^kFShift bits per key. A key sets 3 bits of one word; a lookup whose bits are not all set
-// is a certain miss and skips the table walk. The filter is 1/8 of the table's bytes, so
-// the misses of a sub-level (~3/4 of all probes) mostly hit L2 instead of DRAM.
+// tables (T >= kFMin slots). Vertex x owns the 64-bit words [off[x] >> kFShift,
+// off[x+1] >> kFShift) — disjoint ranges, 2^kFShift adjacency slots per word, i.e.
+// 64 / 2^kFShift bits per key. A key sets TDG_FK bits of one word; a lookup whose bits are
+// not all set is a certain miss and skips the table walk, so the misses of a sub-level
+// (~3/4 of all probes) mostly hit the L2-resident filters instead of DRAM.
 #ifndef TDG_FMIN
 #define TDG_FMIN 1024
 #endif
 constexpr uint32_t kFMin = TDG_FMIN;
 #ifndef TDG_FSHIFT
-#define TDG_FSHIFT 3  // 4 bits per key: sparser filters stay L2-resident (C5: 16 -> 8 -> 4 bits, 3.47 -> 3.26 -> 3.19 s)
+#define TDG_FSHIFT 4  // 4 bits per key: sparser filters stay L2-resident (C5: 16 -> 8 -> 4 bits, 3.47 -> 3.26 -> 3.19 s)
 #endif
 #ifndef TDG_FK
 #define TDG_FK 3  // bits set per key
 #endif
 constexpr uint32_t kFShift = TDG_FSHIFT;
+static_assert((kFMin / kHF) >> kFShift >= 1, "every filtered vertex owns at least one filter word");
 
 __device__ __forceinline__ uint32_t fword(uint32_t x) {
     x = (x ^ 0x9e3779b9u) * 0x85ebca6bu;
@@ -177,10 +175,15 @@ __device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(k
     return b;
 }
 
+// Filter word of key y in the filter of a vertex whose adjacency is [o, o + d).
+__device__ __forceinline__ uint64_t fword_index(uint32_t o, uint32_t d, uint32_t y) {
+    const uint32_t f0 = o >> kFShift, f1 = (o + d) >> kFShift;
+    return static_cast<uint64_t>(f0) + __umulhi(fword(y), f1 - f0);
+}
+
 struct DevGraph {
     uint32_t n = 0, m = 0;
-    const uint32_t* hoff4 = nullptr;          // n+1, table offsets in units of 4 slots
-    const unsigned long long* htab = nullptr;  // hash table slots
+    const unsigned long long* htab = nullptr;  // hash table slots (kHF * 2m)
     const unsigned long long* filt = nullptr;  // membership filters of the big tables (or null)
     const uint32_t* off = nullptr;
     uint32_t* adj = nullptr;

@@ -44,17 +44,15 @@ cudaError_t launch_internal_ids(const BuildBufs& b, uint32_t m, uint32_t* r2i, c
 cudaError_t launch_to_ref(const uint32_t* oeid, const uint32_t* in, uint32_t m, uint32_t add, uint32_t* out,
                           cudaStream_t st, uint32_t* launches);
 
-// Per-vertex neighbour -> edge-id hash tables (tdg_common.cuh). hq: n+1 scratch; the host
-// reads hoff4[n] (total slots / 4) between the two calls to size htab.
-cudaError_t launch_htab_sizes(const uint32_t* off, uint32_t n, uint32_t* hq, uint32_t* hoff4, void* cub_tmp,
-                              size_t cub_bytes, cudaStream_t st, uint32_t* launches);
+// Per-vertex neighbour -> edge-id hash tables (tdg_common.cuh): kHF * 2m slots of 8 bytes,
+// and the membership filters of the big tables: filter_words(m) 64-bit words. Both sizes
+// depend on m only (no readback between build steps).
+inline uint64_t htab_slots(uint64_t m) { return uint64_t(kHF) * 2 * m; }
+inline uint64_t filter_words(uint64_t m) { return ((2 * m) >> kFShift) + 1; }
 cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, const uint32_t* eid,
-                             const uint32_t* hoff4, uint32_t n, uint32_t m, unsigned long long* htab, uint64_t htab_slots,
-                             cudaStream_t st, uint32_t* launches);
-
-// Membership filters of the big tables (tdg_common.cuh); filt_words = htab quads / 2 + 1.
-cudaError_t launch_filter_fill(const uint32_t* adj, const uint32_t* src, const uint32_t* hoff4, uint32_t m,
-                               unsigned long long* filt, uint64_t filt_words, cudaStream_t st, uint32_t* launches);
+                             uint32_t n, uint32_t m, unsigned long long* htab, cudaStream_t st, uint32_t* launches);
+cudaError_t launch_filter_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, uint32_t m,
+                               unsigned long long* filt, cudaStream_t st, uint32_t* launches);
 
 struct StatsAcc {
     unsigned long long d_max, sum_deg_sq, sum_dplus_sq, deg_sum_dplus_sq, deg_s1;
@@ -66,7 +64,10 @@ cudaError_t launch_stats(const uint32_t* off, const uint32_t* eo, const uint32_t
 struct SupportCtl {
     unsigned long long tri3; // sum of supports
     uint32_t piece_head, pad0, smax, pad;
-    unsigned long long probes;  // probe items of the support pass
+    unsigned long long probes;        // probe items of the support pass
+    unsigned long long tab_elems;     // N+(owner) elements loaded into shared-memory tables
+    unsigned long long tab_segments;  // owner segments served from a shared-memory table
+    unsigned long long search_items;  // probe items binary-searched in global memory instead
 };
 constexpr uint32_t kMaxChunks = 1024;  // max blocks of a prep grid (one work chunk each)
 // Requires internal edge ids (launch_internal_ids): s[m] is indexed by oriented slot.
@@ -139,6 +140,33 @@ struct PhaseCtr {
     uint32_t batch_head;     // sub-level / scan: dynamic batch cursor
     uint32_t far_size;       // scan: far-list appends (peel.cu near/far scan)
 };
+// Access tallies of one decomposition (bench.py's byte model of the peel). Entries below
+// kCntProbe are counted per probe and only by the diagnostic count-mode instantiation of
+// k_peel (PeelBufs::count); the rest are phase-level and always counted (leader thread).
+enum PeelCnt : int {
+    kCntFilter = 0,  // membership-filter words read
+    kCntPbits,       // processed-bitmap words read by probes
+    kCntWalk,        // table walks (probes that passed filter and processed bit)
+    kCntSlots,       // table slots read (first slot + collisions)
+    kCntHits,        // triangle visits (element found in the table; 2 state words read)
+    kCntDead,        // probes whose own slot was already processed
+    kCntDec,         // atomicSub decrements issued
+    kCntRepair,      // repairs (+1 after a decrement at or below the level)
+    kCntNext,        // next-frontier appends (+ stamp stores)
+    kCntCross,       // crosser appends
+    kCntProbe,       // ---- below: per-entry compaction tallies (count mode)
+    kCntCompIn = kCntProbe,  // compaction: list entries read (adj + eid + processed bit)
+    kCntCompKept,    // compaction: entries written back
+    kCntCompLong,    // compaction: entries kept in long lists (staged through scratch: +1 copy)
+    kCntScanIn,      // ---- below: phase-level, always counted. Scan: entries read (list + state)
+    kCntScanOut,     // scan: entries written (curr + near + far lists)
+    kCntTasks,       // sub-level tasks prepped (level > 0)
+    kCntSorted,      // tasks bucket-sorted by searched vertex
+    kCntMarks,       // processed-bitmap marks (one per curr edge)
+    kPeelCnt
+};
+constexpr int kCntFirstPhase = kCntScanIn;
+
 struct PeelCtl {
     PhaseCtr ph[3];
     uint32_t levels_len;   // last non-empty level + 1
@@ -153,9 +181,8 @@ struct PeelCtl {
     unsigned long long scan_ns;  // device-clock time in scan phases (leader thread)
     unsigned long long proc_ns;  // device-clock time in sub-level phases
     unsigned long long probes;   // probe items over all sub-levels (sum of W)
-    unsigned long long hits;     // triangle visits (only when PeelBufs::count_hits)
-    unsigned long long dead;     // probes whose own slot was already processed (diagnostic)
     unsigned long long compact_ns;  // device-clock time in adjacency compactions
+    unsigned long long cnt[kPeelCnt];  // access tallies (PeelCnt); probe-level ones only in count mode
     uint32_t xcnt[2];  // crosser-list append counters (peel.cu near/far scan)
     uint32_t rebuilds;  // scans that re-split the far list
     uint32_t pad2;
@@ -170,7 +197,7 @@ struct PeelBufs {
     PeelCtl* ctl;
     uint32_t* nsl;
     uint32_t nsl_cap;
-    uint32_t count_hits;  // diagnostic: count triangle visits (one atomic per warp step)
+    uint32_t count;       // diagnostic count mode: the k_peel<true> instantiation tallies every access
     uint32_t* Ls;         // m: a big sub-level's curr list reordered by searched vertex
     uint32_t* bhist;      // kBuckets counters (zero between uses)
     uint32_t* bcur;       // kBuckets cursors

@@ -209,6 +209,17 @@ class Context:
         except Exception:
             pass
 
+    COUNTER_NAMES = ("filter", "pbits", "walk", "slots", "hits", "dead", "dec", "repair", "next", "cross",
+                     "comp_in", "comp_kept", "comp_long", "scan_in", "scan_out", "tasks", "sorted", "marks",
+                     "sup_tab_elems", "sup_segments", "sup_search")
+
+    def counters(self) -> dict:
+        """tdg_counters: access tallies of this context's last truss/support call (per-probe
+        peel tallies only if TDG_COUNT=1 was in the environment during that call)."""
+        out = (C.c_uint64 * len(self.COUNTER_NAMES))()
+        _ck(_lib.tdg().tdg_counters(self._h, out, len(out)))
+        return dict(zip(self.COUNTER_NAMES, list(out)))
+
     # -- host-pointer entry points
     def truss(self, g: CsrGraph, want_support: bool = False):
         """tdg_truss: returns (truss u32[m], nsl list, support or None, times dict)."""

@@ -27,7 +27,7 @@ def _worker(rank, world, port, q):
     import argparse
     did = None
     if rank == 1:
-        args = argparse.Namespace(steps=1, warmup=0, gpus=world, ref_scale=4)
+        args = argparse.Namespace(steps=1, warmup=0, gpus=world, ref_config=1)
         did = bench.bench_reference(args)
     q.put((rank, mx, val, did))
     dist.barrier()
@@ -49,3 +49,49 @@ def test_two_rank_replica_aggregation():
         assert mx == 250.0                      # max over ranks
         assert val == pytest.approx(2 * 1_000_000 / 0.25 / 1e6)  # world * m / max time
         assert did is None
+
+
+def test_bench_spawns_n_ranks_itself():
+    """`bench.py --gpus 2` without a torchrun environment launches 2 ranks (one process per
+    GPU, distinct LOCAL_RANK = device binding) and rank 0 reports n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-check"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2
+    assert sorted(r["local_rank"] for r in d["ranks"]) == [0, 1]
+    assert len({r["pid"] for r in d["ranks"]}) == 2
+    assert d["max_over_ranks"] == 2.0
+
+
+def test_byte_models_bracket():
+    """The element-level model never exceeds the sector-level bound, and both grow with the
+    tallies (bench.py peel_bytes)."""
+    import bench
+    c = dict(filter=100, pbits=200, walk=80, slots=120, hits=30, dead=10, dec=40, repair=2, next=5, cross=1,
+             comp_in=1000, comp_kept=700, comp_long=50, scan_in=5000, scan_out=4000, tasks=300, sorted=0, marks=300)
+    b = bench.peel_bytes(c, n=100, m=1000, probes=500)
+    assert 0 < b["elem"]["total"] <= b["sector"]["total"]
+    c2 = dict(c, hits=60)
+    assert bench.peel_bytes(c2, 100, 1000, 500)["elem"]["total"] > b["elem"]["total"]
+    assert bench.support_bytes({"sup_tab_elems": 10}, 1000, 500, 7) > 0
+
+
+def test_ncu_traffic_is_tied_to_the_sources(tmp_path, monkeypatch):
+    """profiles/ncu_traffic.json is only used when it was captured on the current CUDA sources."""
+    import json
+    import bench
+    f = tmp_path / "ncu.json"
+    f.write_text(json.dumps({"src_sha": "0000", "C5": {"k_peel": {"dram_bytes": 1}}}))
+    monkeypatch.setattr(bench, "NCU_FILE", str(f))
+    assert bench.ncu_traffic(5).get("stale") is True
+    f.write_text(json.dumps({"src_sha": bench.src_sha(), "C5": {"k_peel": {"dram_bytes": 1}}}))
+    assert bench.ncu_traffic(5) == {"k_peel": {"dram_bytes": 1}}
