@@ -16,6 +16,7 @@
  *   tdg_triangle_count   <- trussdec::triangle_count(const TrussGraph&, int)  triangle.cpp:90-116
  *   tdg_ktruss_components<- trussdec::ktruss_subgraphs(tg, res, k)  truss_serial.cpp:176-210
  *   tdg_canonicalize     <- trussdec::canonicalize(const RawEdgeList&)  graph.cpp:19-71
+ *   tdg_read_edge_list   <- trussdec::read_edge_list(const std::string&) graph.cpp:152-200
  *   tdg_kcore / tdg_coreness_order / tdg_reorder
  *                        <- kcore_parallel / coreness_order (kcore.cpp:68-138), reorder (graph.cpp:103-133)
  *   tdg_scan             <- trussdec::scan(...)              truss_parallel.hpp:62, .cpp:21-37
@@ -55,6 +56,8 @@ extern "C" {
 #define TDG_ERR_CUDA (-2)      /* CUDA runtime error or no usable device                  */
 #define TDG_ERR_NOMEM (-3)     /* device or pinned allocation failed (std::bad_alloc)    */
 #define TDG_ERR_RANGE (-4)     /* graph exceeds 32-bit edge width (graph.cpp:48-49)      */
+#define TDG_ERR_IO (-5)        /* file cannot be opened / read, or malformed edge-list text
+                                  (the reference's std::runtime_error, graph.cpp:153-186)   */
 
 typedef struct tdg_context tdg_context;
 
@@ -166,6 +169,14 @@ int tdg_reorder(tdg_context* ctx, const tdg_csr* g, const uint32_t* perm, int64_
  * Capacities: offsets 2*npairs+1, neighbors 2*npairs, labels 2*npairs. Host pointers. */
 int tdg_canonicalize(tdg_context* ctx, const uint64_t* pairs, uint64_t npairs, int64_t* offsets,
                      int32_t* neighbors, uint64_t* labels, int64_t* n_out, int64_t* m_out);
+
+/* read_edge_list (graph.cpp:152-200): the text edge list at `path` (plain or gzip, read and
+ * inflated with zlib on the host, parsed on the GPU) as raw label pairs in file order:
+ * *pairs_out = malloc'd host array of 2 * *npairs uint64 (u0, v0, u1, v1, ...; release with
+ * tdg_free). Errors are TDG_ERR_IO with the reference's message ("cannot open input file:
+ * <path>" or "<path>:<line>: <why>" for the first malformed line). */
+int tdg_read_edge_list(tdg_context* ctx, const char* path, uint64_t** pairs_out, uint64_t* npairs);
+void tdg_free(void* p);
 
 /* stats (host-pointer graph). */
 int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out);

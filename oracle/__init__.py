@@ -221,6 +221,7 @@ class Reference:
         L.ref_prepare.restype = C.c_void_p
         L.ref_run.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_uint32)]
         L.ref_free.argtypes = [C.c_void_p]
+        L.ref_read_edge_list.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         L.ref_support_am4.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, C.c_int, _u32p]
         L.ref_build_truss_graph.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p, _u32p, _u32p]
         L.ref_truss_wc.argtypes = [C.c_int64, C.c_int64, _i64p, _i32p, _u32p]
@@ -280,6 +281,16 @@ class Reference:
 
     def free(self, h):
         self.lib.ref_free(h)
+
+    def read_edge_list(self, path: str) -> np.ndarray:
+        """graph.cpp:152-200: (k, 2) uint64 pairs; raises RuntimeError with the reference's message."""
+        k = C.c_uint64()
+        buf = np.zeros(2 * 1024, np.uint64)
+        self._check(self.lib.ref_read_edge_list(os.fsencode(path), buf.ctypes.data, 1024, C.byref(k)))
+        if k.value > 1024:
+            buf = np.zeros(2 * k.value, np.uint64)
+            self._check(self.lib.ref_read_edge_list(os.fsencode(path), buf.ctypes.data, k.value, C.byref(k)))
+        return buf[: 2 * k.value].reshape(-1, 2)
 
     def support_am4(self, g: Csr, workers: int = 1) -> np.ndarray:
         s = np.zeros(max(g.m, 1), np.uint32)

@@ -265,6 +265,20 @@ int ref_reorder(int64_t n, int64_t m, const int64_t* off, const int32_t* nb, con
     });
 }
 
+// read_edge_list (graph.cpp:152-200): pairs into a caller buffer of cap pairs; *npairs is
+// the file's pair count (also when it exceeds cap: call again with a bigger buffer).
+int ref_read_edge_list(const char* path, uint64_t* pairs, uint64_t cap, uint64_t* npairs) {
+    return guarded([&] {
+        RawEdgeList raw = read_edge_list(path);
+        *npairs = raw.edges.size();
+        for (uint64_t i = 0; i < raw.edges.size() && i < cap; i++) {
+            pairs[2 * i] = raw.edges[i].first;
+            pairs[2 * i + 1] = raw.edges[i].second;
+        }
+        return 0;
+    });
+}
+
 // Fixture graphs exactly as the reference tests build them (tests/helpers.hpp:12-43):
 // kind 0 = er_graph(n, p, seed), kind 1 = rmat_graph(scale=n, ef=(int)p, seed),
 // kind 2 = canonicalize(pairs). CSR written into caller buffers (capacities given).

@@ -16,7 +16,7 @@ LIB_DIR = os.path.join(PKG_DIR, "lib")
 CSRC_DIR = os.path.join(PKG_DIR, "csrc")
 TDG_SO = os.path.join(LIB_DIR, "libtdg.so")
 
-TDG_OK, TDG_ERR_INVALID, TDG_ERR_CUDA, TDG_ERR_NOMEM, TDG_ERR_RANGE = 0, -1, -2, -3, -4
+TDG_OK, TDG_ERR_INVALID, TDG_ERR_CUDA, TDG_ERR_NOMEM, TDG_ERR_RANGE, TDG_ERR_IO = 0, -1, -2, -3, -4, -5
 
 _lock = threading.Lock()
 _TDG = None
@@ -85,6 +85,8 @@ SIGNATURES = [
     ("tdg_kcore", _i32, [_vp, _P(tdg_csr), _vp, _P(_u32)]),
     ("tdg_coreness_order", _i32, [_vp, _u64, _vp, _vp]),
     ("tdg_reorder", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp]),
+    ("tdg_read_edge_list", _i32, [_vp, C.c_char_p, _P(_P(_u64)), _P(_u64)]),
+    ("tdg_free", None, [_vp]),
     ("tdg_canonicalize", _i32, [_vp, _vp, _u64, _vp, _vp, _vp, _P(C.c_int64), _P(C.c_int64)]),
     ("tdg_scan", _i32, [_vp, _vp, _u64, _u32, _vp, _vp, _vp, _P(_u64)]),
     ("tdg_process_sublevel", _i32, [_vp, _P(tdg_csr), _vp, _u32, _vp, _u64, _vp, _vp, _vp, _vp, _P(_u64)]),

@@ -13,6 +13,8 @@
 #include <vector>
 #include <algorithm>
 
+#include <zlib.h>
+
 #include "tdg.h"
 #include "tdg_kernels.h"
 
@@ -92,7 +94,7 @@ struct tdg_context {
     // it (they are never live at the same time; layout in ensure_arena)
     DevBuf arena;
     DevBuf cchunk, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, bhist, bcur, trace;
-    DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing;
+    DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing, ptext, pscr, ppairs;
     // arena views (recomputed by ensure_arena)
     uint32_t *src = nullptr, *flag = nullptr, *pos = nullptr, *oadj = nullptr, *osrc = nullptr, *stask = nullptr,
              *sx = nullptr, *s = nullptr, *L0 = nullptr, *L1 = nullptr, *Ls = nullptr, *A0 = nullptr, *A1 = nullptr,
@@ -260,7 +262,7 @@ struct tdg_context {
         DevBuf* all[] = {&off64, &off, &adj, &eo, &up, &P, &eid, &el, &opos, &oeid, &sbeg, &dl, &pbits, &htab, &filt,
                          &arena, &cchunk, &nsl, &ctl, &sctl, &sacc, &cub, &truss, &sup, &f0, &f1, &f2, &bsum, &bhist,
                          &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1, &kwpre, &kctl, &ktmp, &knoff, &knadj,
-                         &kperm, &kbad, &ing};
+                         &kperm, &kbad, &ing, &ptext, &pscr, &ppairs};
         for (DevBuf* b : all) b->release();
         word = 0;
     }
@@ -829,6 +831,90 @@ int tdg_canonicalize(tdg_context* ctx, const uint64_t* pairs, uint64_t npairs, i
         *m_out = static_cast<int64_t>(m);
     });
 }
+
+int tdg_read_edge_list(tdg_context* ctx, const char* path, uint64_t** pairs_out, uint64_t* npairs) {
+    return guarded([&] {
+        if (!path || !pairs_out || !npairs) throw Fail{TDG_ERR_INVALID, "NULL argument"};
+        *pairs_out = nullptr;
+        *npairs = 0;
+        const std::string p(path);
+        // host: read / inflate (gzopen reads plain text too, as the reference)
+        gzFile f = gzopen(path, "rb");
+        if (!f) throw Fail{TDG_ERR_IO, "cannot open input file: " + p};
+        std::vector<unsigned char> text;
+        for (;;) {
+            const size_t at = text.size(), blk = size_t(64) << 20;
+            text.resize(at + blk);
+            const int r = gzread(f, text.data() + at, static_cast<unsigned>(blk));
+            if (r < 0) {
+                gzclose(f);
+                throw Fail{TDG_ERR_IO, "read error: " + p};
+            }
+            text.resize(at + static_cast<size_t>(r));
+            if (static_cast<size_t>(r) < blk) break;
+        }
+        gzclose(f);
+        tdg_context* c = resolve(ctx);
+        c->use();
+        c->launches = 0;
+        // GPU: parse chunks of <= 1 GiB cut after a '\n' (segment counts stay 32-bit)
+        std::vector<uint64_t> out;
+        const size_t N = text.size(), kChunk = size_t(1) << 30;
+        for (size_t c0 = 0; c0 < N;) {
+            size_t c1 = std::min(N, c0 + kChunk);
+            if (c1 < N) {
+                while (c1 > c0 && text[c1 - 1] != '\n') c1--;
+                if (c1 == c0) throw Fail{TDG_ERR_IO, p + ": line longer than 1 GiB"};
+            }
+            const uint64_t nb = c1 - c0, nseg = (nb + 255) / 256;
+            c->ptext.ensure(nb, "edge-list text");
+            const size_t sb = parse_scratch_bytes(nb);
+            c->pscr.ensure(sb + 8, "parse scratch");
+            auto* err = reinterpret_cast<unsigned long long*>(c->pscr.as<char>() + (c->pscr.cap - 8));
+            ck(cudaMemcpyAsync(c->ptext.p, text.data() + c0, nb, cudaMemcpyHostToDevice, c->stream), "H2D text");
+            ck(launch_parse_count(c->ptext.as<unsigned char>(), nb, c->pscr.p, c->pscr.cap - 8, err, c->stream,
+                                  &c->launches), "parse kernels");
+            unsigned long long e = 0;
+            uint32_t total = 0;
+            d2h(c->stream, &e, err, 8, "D2H parse status");
+            if (e != ~0ull) {
+                const size_t pos = c0 + static_cast<size_t>(e >> 2);
+                const uint64_t lineno = 1 + static_cast<uint64_t>(std::count(text.begin(), text.begin() + pos, '\n'));
+                std::string why;
+                switch (static_cast<uint32_t>(e & 3)) {
+                    case kParseNegative: why = "negative vertex label"; break;
+                    case kParseTrailing: why = "trailing characters after edge"; break;
+                    default: {
+                        size_t q = pos;
+                        while (q < N && text[q] != '\n') q++;
+                        why = "expected two nonnegative integers, got '" +
+                              std::string(reinterpret_cast<const char*>(text.data() + pos), q - pos) + "'";
+                    }
+                }
+                throw Fail{TDG_ERR_IO, p + ":" + std::to_string(lineno) + ": " + why};
+            }
+            d2h(c->stream, &total, c->pscr.as<uint32_t>() + 2 * nseg + 1, 4, "D2H edge count");
+            if (total) {
+                c->ppairs.ensure(size_t(total) * 16, "edge pairs");
+                ck(launch_parse_write(c->ptext.as<unsigned char>(), nb, c->pscr.p, c->ppairs.as<unsigned long long>(),
+                                      c->stream, &c->launches), "parse kernels");
+                const size_t at = out.size();
+                out.resize(at + 2 * size_t(total));
+                d2h(c->stream, out.data() + at, c->ppairs.p, size_t(total) * 16, "D2H edge pairs");
+            }
+            c0 = c1;
+        }
+        if (!out.empty()) {
+            auto* h = static_cast<uint64_t*>(std::malloc(out.size() * 8));
+            if (!h) throw std::bad_alloc();
+            std::memcpy(h, out.data(), out.size() * 8);
+            *pairs_out = h;
+        }
+        *npairs = out.size() / 2;
+    });
+}
+
+void tdg_free(void* p) { std::free(p); }
 
 int tdg_stats(tdg_context* ctx, const tdg_csr* g, tdg_graph_stats* out) {
     return guarded([&] {

@@ -130,6 +130,18 @@ size_t ingest_cub_bytes(uint64_t npairs);
 cudaError_t launch_ingest(const IngestBufs& B, uint64_t npairs, cudaStream_t st, uint64_t* n_out, uint64_t* m_out,
                           uint32_t* launches);
 
+// ---- text edge-list parsing (graph.cpp:152-200 read_edge_list), edgelist.cu ----
+enum ParseError : uint32_t { kParseNegative = 0, kParseExpected = 1, kParseTrailing = 2 };
+size_t parse_scratch_bytes(uint64_t nbytes);
+// Pass 1 over nbytes of text (< 2^31): per-segment edge counts + their exclusive scan in
+// scratch (total edges at u32 index 2 * nseg + 1, nseg = ceil(nbytes / 256)); *err = min over
+// failing lines of (line start << 2 | ParseError), or ~0.
+cudaError_t launch_parse_count(const unsigned char* text, uint64_t nbytes, void* scratch, size_t scratch_bytes,
+                               unsigned long long* err, cudaStream_t st, uint32_t* launches);
+// Pass 2: the (u, v) pairs in file order (2 x u64 each).
+cudaError_t launch_parse_write(const unsigned char* text, uint64_t nbytes, void* scratch, unsigned long long* pairs,
+                               cudaStream_t st, uint32_t* launches);
+
 // ---- peel (truss_parallel.cpp:21-150 equivalent) ----
 struct PhaseCtr {
     unsigned long long work; // sub-level: total probe items (informational)

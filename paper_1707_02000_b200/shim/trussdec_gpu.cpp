@@ -25,6 +25,38 @@ void raise_status(int status) {
     throw std::runtime_error(msg);
 }
 
+RawEdgeList read_edge_list(const std::string& path) {
+    std::uint64_t* pairs = nullptr;
+    std::uint64_t k = 0;
+    check(tdg_read_edge_list(default_context(), path.c_str(), &pairs, &k));
+    RawEdgeList raw;
+    raw.edges.resize(k);
+    for (std::uint64_t i = 0; i < k; i++) raw.edges[i] = {pairs[2 * i], pairs[2 * i + 1]};
+    tdg_free(pairs);
+    return raw;
+}
+
+CsrGraph canonicalize(const RawEdgeList& raw) {
+    const std::uint64_t k = raw.edges.size();
+    std::vector<std::uint64_t> flat(2 * k + 2);
+    for (std::uint64_t i = 0; i < k; i++) {
+        flat[2 * i] = raw.edges[i].first;
+        flat[2 * i + 1] = raw.edges[i].second;
+    }
+    std::vector<std::int64_t> off(2 * k + 2);
+    std::vector<std::int32_t> nb(2 * k + 1);
+    std::vector<std::uint64_t> lab(2 * k + 1);
+    std::int64_t n = 0, m = 0;
+    check(tdg_canonicalize(default_context(), flat.data(), k, off.data(), nb.data(), lab.data(), &n, &m));
+    CsrGraph g;
+    g.n = static_cast<std::uint32_t>(n);
+    g.m = static_cast<std::uint32_t>(m);
+    g.offsets.assign(off.begin(), off.begin() + n + 1);
+    g.neighbors.assign(nb.begin(), nb.begin() + 2 * m);
+    g.labels.assign(lab.begin(), lab.begin() + n);
+    return g;
+}
+
 TrussGraph build_truss_graph(const CsrGraph& g) {
     TrussGraph tg;
     tg.csr = g;

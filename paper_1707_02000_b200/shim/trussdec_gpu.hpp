@@ -53,6 +53,10 @@ struct CsrGraph {
     std::uint64_t label_of(VertexId u) const { return labels.empty() ? u : labels[u]; }
 };
 
+struct RawEdgeList {  // graph.hpp:13-15
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> edges;
+};
+
 struct TrussGraph {
     CsrGraph csr;
     std::vector<EdgeId> eid;
@@ -183,6 +187,8 @@ CsrGraph reorder(const CsrGraph& g, const std::vector<VertexId>& perm);         
 std::uint64_t triangle_count(const TrussGraph& tg, int workers);  // triangle.hpp:19
 std::vector<std::vector<EdgeId>> ktruss_subgraphs(const TrussGraph& tg, const TrussnessResult& res,
                                                   std::uint32_t k);  // truss_serial.hpp:43-45
+RawEdgeList read_edge_list(const std::string& path);  // graph.hpp:78 (GPU-parsed)
+CsrGraph canonicalize(const RawEdgeList& raw);         // graph.hpp:69 (GPU)
 TrussGraph build_truss_graph(const CsrGraph& g);
 GraphStats stats(const CsrGraph& g);
 SupportArray support_am4(const TrussGraph& tg, int workers);

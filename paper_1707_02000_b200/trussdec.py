@@ -21,6 +21,7 @@ Arrays are numpy (uint32 per-edge, int64 offsets, int32 neighbours).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from dataclasses import dataclass, field
 
@@ -411,6 +412,23 @@ def reorder(g: CsrGraph, perm) -> CsrGraph:
         labels = np.empty_like(g.labels)
         labels[p] = g.labels
     return CsrGraph(g.n, g.m, off, nb[: 2 * g.m], labels)
+
+
+def read_edge_list(path: str) -> np.ndarray:
+    """graph.cpp:152-200 (tdg_read_edge_list): the text edge list at `path` (plain or gzip;
+    '#' / '%' comment lines, blank lines, any whitespace) as raw label pairs, shape (k, 2)
+    uint64, in file order. Parsed on the GPU; raises RuntimeError with the reference's
+    message ("<path>:<line>: <why>") on malformed input."""
+    pairs = C.POINTER(C.c_uint64)()
+    k = C.c_uint64()
+    L = _lib.tdg()
+    _ck(L.tdg_read_edge_list(default_context().handle, os.fsencode(path), C.byref(pairs), C.byref(k)))
+    try:
+        out = np.ctypeslib.as_array(pairs, shape=(2 * k.value,)).copy() if k.value else np.zeros(0, np.uint64)
+    finally:
+        if pairs:
+            L.tdg_free(pairs)
+    return out.reshape(-1, 2)
 
 
 def canonicalize(pairs) -> CsrGraph:
