@@ -20,6 +20,45 @@ def _build() -> str:
     return exe
 
 
+REF_INC = "/root/reference/proj/include"
+REFTYPES_EXE = os.path.join(ROOT, "tests", "cpp", "build", "test_shim_reftypes")
+
+
+def build_reftypes() -> str | None:
+    """The reference-type drop-in test (tests/cpp/test_shim_reftypes.cpp) needs the reference
+    headers, so it is compiled where /root/reference exists (here, and by
+    __graft_entry__.build()); the binary travels to the GPU box with oracle/_ref."""
+    from oracle import REF_SO
+    from paper_1707_02000_b200._lib import LIB_DIR, ensure_built
+    if not (os.path.isdir(REF_INC) and os.path.exists(REF_SO)):
+        return REFTYPES_EXE if os.path.exists(REFTYPES_EXE) else None
+    ensure_built()
+    os.makedirs(os.path.dirname(REFTYPES_EXE), exist_ok=True)
+    ref_dir = os.path.dirname(REF_SO)
+    subprocess.run(["/usr/bin/g++", "-O1", "-std=c++20", f"-I{REF_INC}", f"-I{ROOT}/include",
+                    f"-I{ROOT}/paper_1707_02000_b200/shim", os.path.join(ROOT, "tests", "cpp", "test_shim_reftypes.cpp"),
+                    f"-L{LIB_DIR}", "-ltrussdec_gpu", "-ltdg", f"-L{ref_dir}", "-l:libtrussdec_ref.so", "-fopenmp",
+                    f"-Wl,-rpath,{LIB_DIR}", f"-Wl,-rpath,{ref_dir}", "-o", REFTYPES_EXE], check=True)
+    return REFTYPES_EXE
+
+
+def test_reftypes_shim_compiles_against_reference_headers():
+    if not os.path.isdir(REF_INC):
+        pytest.skip("reference headers absent (GPU box): the binary is prebuilt where they exist")
+    assert build_reftypes() is not None
+
+
+@pytest.mark.gpu
+def test_shim_on_reference_types_on_gpu():
+    """truss_parallel_as<trussdec::ParallelDecomposition> on trussdec::TrussGraph built by the
+    reference library: bit-identical truss, nsl, barriers, k-classes and supports."""
+    exe = build_reftypes()
+    assert exe is not None, "tests/cpp/build/test_shim_reftypes was not prebuilt (build() where /root/reference exists)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all reference-type shim checks passed" in r.stdout
+
+
 def test_shim_compiles_and_links():
     assert os.path.exists(_build())
 
