@@ -14,7 +14,9 @@ import threading
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(PKG_DIR, "lib")
 CSRC_DIR = os.path.join(PKG_DIR, "csrc")
-TDG_SO = os.path.join(LIB_DIR, "libtdg.so")
+# TDG_SO in the environment selects another build of the same library (A/B variants built
+# with scripts/variants.sh under lib_variants/; measurement only)
+TDG_SO = os.environ.get("TDG_SO") or os.path.join(LIB_DIR, "libtdg.so")
 
 TDG_OK, TDG_ERR_INVALID, TDG_ERR_CUDA, TDG_ERR_NOMEM, TDG_ERR_RANGE, TDG_ERR_IO = 0, -1, -2, -3, -4, -5
 

@@ -166,6 +166,8 @@ enum PeelCnt : int {
     kCntRepair,      // repairs (+1 after a decrement at or below the level)
     kCntNext,        // next-frontier appends (+ stamp stores)
     kCntCross,       // crosser appends
+    kCntMerge,       // merge-task diagonal steps (also part of the probe total W)
+    kCntMergeLoad,   // merge-task list elements staged into shared memory
     kCntProbe,       // ---- below: per-entry compaction tallies (count mode)
     kCntCompIn = kCntProbe,  // compaction: list entries read (adj + eid + processed bit)
     kCntCompKept,    // compaction: entries written back
