@@ -185,6 +185,25 @@ def survey_bytes(S1: int, S2: int, T: int, m: int, sum_tau_m1: int) -> tuple[int
     return 4 * S1 + 24 * m + 32 * T, 4 * S2 + 48 * T + 55 * m + 5 * sum_tau_m1
 
 
+REF_HOST = os.path.join(ROOT, "profiles", "r02_ref_host.jsonl")
+
+
+def reference_host_record(cfg: int, variant: str = "ii") -> dict | None:
+    """The reference's full run on this config on the GPU box's host, recorded once
+    (scripts/ref_host_run.py -> profiles/r02_ref_host.jsonl): the workload itself is too slow
+    for every bench run (C5: ~52 min on 16 cores)."""
+    try:
+        for line in open(REF_HOST):
+            d = json.loads(line)
+            if d["config"] == cfg and d["variant"] == variant:
+                return {"value": d["engine_medges_s"], "unit": UNIT, "engine_s": d["engine_s"], "threads": d["threads"],
+                        "cpu": d.get("cpu"), "phases_s": d["phases_s"], "variant": variant,
+                        "source": "profiles/r02_ref_host.jsonl (scripts/ref_host_run.py on the GPU box host)"}
+    except Exception:
+        return None
+    return None
+
+
 def ncu_traffic(cfg: int) -> dict | None:
     """ncu DRAM bytes per launch for this config, if profiles/ncu_traffic.json was captured
     on the current CUDA sources (src_sha match); else None."""
@@ -256,6 +275,7 @@ def bench_reference(args):
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "prep_s": prep,
+            "c5_reference_host": reference_host_record(5),
             "phases_s": {k: float(np.median([r[k] for r in runs])) for k in ("support", "scan", "processing", "engine")},
             "t_max": runs[-1]["t_max"], "t_max_golden": gold and gold.get("t_max"),
             "omp": {k: os.environ.get(k) for k in ("OMP_PROC_BIND", "OMP_PLACES")}}
@@ -512,6 +532,7 @@ def bench_ours(args):
                    "gpu_same_config": gpu_pair,
                    "speedup_same_config": {"vs_i": gpu_pair["value"] / ref["i"]["value"],
                                            "vs_ii": gpu_pair["value"] / ref["ii"]["value"]},
+                   "workload_reference_host": reference_host_record(args.config),
                    "omp": {k: os.environ.get(k) for k in ("OMP_PROC_BIND", "OMP_PLACES")}}
         except Exception as e:  # the checker is optional on a box without oracle/_ref
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}

@@ -211,8 +211,6 @@ enum {
     TDG_CNT_REPAIR,         /* peel: repairs (truss_parallel.cpp:58-62)                    */
     TDG_CNT_NEXT,           /* peel: next-frontier appends (truss_parallel.cpp:55-57)      */
     TDG_CNT_CROSS,          /* peel: near/far crosser appends                              */
-    TDG_CNT_MERGE,          /* peel: merge-task diagonal steps (part of the probe total)   */
-    TDG_CNT_MERGE_LOAD,     /* peel: merge-task list elements staged in shared memory      */
     TDG_CNT_COMP_IN,        /* peel: adjacency-compaction entries read                     */
     TDG_CNT_COMP_KEPT,      /* peel: compaction entries written back (short lists)         */
     TDG_CNT_COMP_LONG,      /* peel: compaction entries kept in long lists (two copies)    */

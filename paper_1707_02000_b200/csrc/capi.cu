@@ -467,10 +467,10 @@ void fill_times(tdg_times* t, tdg_context* c, bool host, bool peel) {
 int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t* support_out,
                uint32_t* nsl_out, uint64_t nsl_cap, uint64_t* nsl_len, tdg_times* times, bool host) {
     return guarded([&] {
-        if (!truss_out) throw Fail{TDG_ERR_INVALID, "truss_out is NULL"};
         tdg_context* c = resolve(ctx);
         c->use();
         const Dims d = check_graph(g, host);
+        if (!truss_out && d.m) throw Fail{TDG_ERR_INVALID, "truss_out is NULL"};
         c->launches = 0;
         stage_and_build(c, g, d, host, true, true, true);
         c->ensure_peel(d.n, d.m);
@@ -538,10 +538,10 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
 
 int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times, bool host) {
     return guarded([&] {
-        if (!support_out) throw Fail{TDG_ERR_INVALID, "support_out is NULL"};
         tdg_context* c = resolve(ctx);
         c->use();
         const Dims d = check_graph(g, host);
+        if (!support_out && d.m) throw Fail{TDG_ERR_INVALID, "support_out is NULL"};
         c->launches = 0;
         stage_and_build(c, g, d, host, true, false, true);
         const DevGraph dg = c->dev_graph(d.n, d.m);

@@ -14,17 +14,9 @@
 // `visit(active, hit, task, ja, e)`; all 32 lanes call them together (warp collectives ok).
 #pragma once
 
-#include <type_traits>
-
 #include "tdg_common.cuh"
 
 namespace tdg {
-
-// Policy::kHasStaged (default false): the policy has STAGED tasks run by staged_range().
-template <class P, class = void>
-struct has_staged : std::false_type {};
-template <class P>
-struct has_staged<P, std::void_t<decltype(P::kHasStaged)>> : std::bool_constant<P::kHasStaged> {};
 
 struct ITask {
     uint32_t id;      // peel: e1 ; support: edge id of the oriented edge a->b
@@ -173,25 +165,7 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
             end_held = shfl64(s32, 31);
             held = i;
         }
-        unsigned long long limit = x1 < end_held ? x1 : end_held;
-        if constexpr (has_staged<Policy>::value) {
-            // STAGED tasks (the peel's merge tasks) run alone over their in-piece range; the
-            // window below stops at the first staged task it holds.
-            const uint32_t smask = __ballot_sync(kFull, P.staged(k));
-            if (smask & 1u) {
-                const unsigned long long st0 = shfl64(st, 0), st1 = shfl64(st, 1);
-                const unsigned long long end0 = st1 < end_held ? st1 : end_held;
-                const unsigned long long lim0 = x1 < end0 ? x1 : end0;
-                P.staged_range(shfl_task(k, 0), static_cast<uint32_t>(base - st0), static_cast<uint32_t>(lim0 - st0));
-                if (lim0 == end0) i += 1;
-                base = lim0;
-                continue;
-            }
-            if (smask) {
-                const unsigned long long sm = shfl64(st, __ffs(smask) - 1);
-                limit = sm < limit ? sm : limit;
-            }
-        }
+        const unsigned long long limit = x1 < end_held ? x1 : end_held;
         const uint32_t relk = st <= base ? 0u
                               : (st - base > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(st - base));
         constexpr int U = Policy::kUnroll;

@@ -69,21 +69,7 @@ constexpr int kWarps = kPeelThreads / 32;
 #ifndef TDG_PEEL_FAST
 #define TDG_PEEL_FAST 0  // engine fast path (intersect.cuh) for the peel's probe loop
 #endif
-// MERGE tasks: when both live lists are long and of comparable length, N(u) ∩ N(v) is a
-// merge-path intersection of the two sorted live lists (coalesced streams, no table or filter
-// lookups); the task's work axis is then its la + lb merge diagonal (PeelPolicy::staged_range).
-#ifndef TDG_MERGE_RATIO
-#define TDG_MERGE_RATIO 4  // merge if lb <= RATIO * la (0 = hash lookups only)
-#endif
-#ifndef TDG_MERGE_MIN
-#define TDG_MERGE_MIN 256  // ... and la >= MIN live entries
-#endif
-constexpr uint32_t kMerge = 0x80000000u;  // flag in ITask::lb (lb < 2^31: 2m < 2^32)
-constexpr int kMergeK = 8;                // merge diagonal steps per lane per chunk
-constexpr uint32_t kMergeC = 32 * kMergeK;
-
-// HASH task: ob = off[b], lb = d(b) (the table is kHF * d(b) slots at slot kHF * off[b]).
-// MERGE task: ob = off[b], lb = dl[b] | kMerge (b's live list).
+// ob = off[b], lb = d(b) (b's table: kHF * d(b) slots at slot kHF * off[b]).
 __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
     const uint2 p = g.el[e1];
     const uint32_t du = g.dl[p.x], dv = g.dl[p.y];
@@ -95,16 +81,8 @@ __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
     k.la = pu ? du : dv;
     k.aux = b;
     k.ob = g.off[b];
-    const uint32_t lbl = pu ? dv : du;
-    if (TDG_MERGE_RATIO && k.la >= TDG_MERGE_MIN && static_cast<uint64_t>(lbl) <= uint64_t(TDG_MERGE_RATIO) * k.la)
-        k.lb = lbl | kMerge;
-    else
-        k.lb = g.off[b + 1] - k.ob;
+    k.lb = g.off[b + 1] - k.ob;
     return k;
-}
-// items of a task on the sub-level's work axis: probes (hash) or merge diagonal steps
-__device__ __forceinline__ uint32_t task_work(const ITask& k) {
-    return (k.lb & kMerge) ? k.la + (k.lb & ~kMerge) : k.la;
 }
 
 __device__ __forceinline__ void reset_ctr(PhaseCtr* c) {
@@ -175,12 +153,10 @@ struct PeelPolicy {
     uint32_t* xcnt;
     const uint32_t* pbits;        // edges processed in earlier sub-levels (or null)
     const uint4* desc;            // task descriptors written by phase_prep
-    uint32_t* mbuf;               // this warp's 2 x kMergeC shared-memory merge window
     static constexpr bool kFast = TDG_PEEL_FAST;
     static constexpr int kUnroll = TDG_PEEL_U;
-    static constexpr bool kHasStaged = TDG_MERGE_RATIO != 0;
     static_assert(kUnroll > 1, "the peel's probe loop is the U-chain form (run)");
-    __device__ bool staged(const ITask& k) const { return (k.lb & kMerge) != 0; }
+
     __device__ ITask load(uint32_t t) const {
         // (aux = kNone: b's own id never occurs in its table, only a filter miss is lost)
         const uint4 d = desc[t];
@@ -244,107 +220,6 @@ struct PeelPolicy {
         }
         emit_many(o, &ph->out_size, next);
         emit_many(c, xcnt, X);
-    }
-    // ---- MERGE tasks: the diagonal range [d0, d1) of the merge path of the two sorted live
-    // lists A = N(a) and B = N(b) (ties take A first: a common element w is found when A's copy
-    // is taken, against B's current element). Per chunk of kMergeC diagonal steps the warp
-    // stages the chunk's A and B windows in shared memory (coalesced), each lane merges
-    // kMergeK steps from its own split, and the chunk's common elements (triangles {a, b, w})
-    // go through the same visit logic as hash hits (apply).
-    static __device__ __forceinline__ uint32_t split_smem(const uint32_t* sA, uint32_t na, const uint32_t* sB,
-                                                          uint32_t nb, uint32_t d) {
-        uint32_t lo = d > nb ? d - nb : 0u, hi = d < na ? d : na;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (sA[mid] <= sB[d - 1 - mid]) lo = mid + 1; else hi = mid;
-        }
-        return lo;
-    }
-    // Same split on global memory, warp-cooperative (32 probes per round; all lanes call).
-    static __device__ __forceinline__ uint32_t split_global(const uint32_t* A, uint32_t na, const uint32_t* B,
-                                                            uint32_t nb, uint32_t d) {
-        const uint32_t lane = lane_id();
-        uint32_t lo = d > nb ? d - nb : 0u, hi = d < na ? d : na;  // answer in [lo, hi]
-        while (lo < hi) {
-            const uint32_t span = hi - lo;
-            const uint32_t step = span > 32 ? (span + 31) / 32 : 1u;
-            const uint32_t i = lo + lane * step;
-            const bool f = i < hi && A[i] <= B[d - 1 - i];  // true for i < answer
-            const uint32_t c = __popc(__ballot_sync(kFull, f));
-            if (step == 1) return lo + c;
-            const uint32_t nlo = c ? lo + (c - 1) * step + 1 : lo;
-            hi = min(hi, lo + c * step);
-            lo = nlo;
-        }
-        return lo;
-    }
-    __device__ void staged_range(const ITask& k, uint32_t d0, uint32_t d1) const {
-        const uint32_t lane = lane_id();
-        const uint32_t na = k.la, nb = k.lb & ~kMerge;
-        const uint32_t* A = g.adj + k.oa;
-        const uint32_t* Bv = g.adj + k.ob;
-        uint32_t* sA = mbuf;
-        uint32_t* sB = mbuf + kMergeC;
-        uint32_t ia = split_global(A, na, Bv, nb, d0);
-        uint32_t ib = d0 - ia;
-        for (uint32_t d = d0; d < d1;) {
-            const uint32_t dc = min(kMergeC, d1 - d);
-            const uint32_t ca = min(dc, na - ia), cb = min(dc, nb - ib);
-            __syncwarp();
-            for (uint32_t q = lane; q < ca; q += 32) sA[q] = A[ia + q];
-            for (uint32_t q = lane; q < cb; q += 32) sB[q] = Bv[ib + q];
-            __syncwarp();
-            const uint32_t s0 = min(lane * uint32_t(kMergeK), dc), s1 = min(s0 + uint32_t(kMergeK), dc);
-            uint32_t i = split_smem(sA, ca, sB, cb, s0), j = s0 - i;
-            constexpr int M = kMergeK / 2;  // at most one common element per two steps
-            uint32_t ea[M], eb[M], ids[M];
-            int nm = 0;
-#pragma unroll
-            for (int q = 0; q < M; q++) {
-                ea[q] = kNone;
-                eb[q] = kNone;
-                ids[q] = k.id;
-            }
-            for (uint32_t t = s0; t < s1; t++) {
-                const uint32_t av = i < ca ? sA[i] : 0xffffffffu;
-                const uint32_t bv = j < cb ? sB[j] : 0xffffffffu;
-                if (i < ca && (j >= cb || av <= bv)) {
-                    if (av == bv && j < cb) {
-#pragma unroll
-                        for (int q = 0; q < M; q++)
-                            if (q == nm) { ea[q] = ia + i; eb[q] = ib + j; }
-                        nm++;
-                    }
-                    i++;
-                } else {
-                    j++;
-                }
-            }
-            // list slots -> edge ids of the two peers (a, w) and (b, w)
-#pragma unroll
-            for (int q = 0; q < M; q++) {
-                if (eb[q] != kNone) {
-                    ea[q] = g.eid[k.oa + ea[q]];
-                    eb[q] = g.eid[k.ob + eb[q]];
-                }
-            }
-            uint32_t cn[kCntProbe] = {};
-            apply<M>(ea, eb, ids, cn);
-            if constexpr (kCount) {
-                if (lane == 0) {
-                    cn[kCntMerge] += dc;
-                    cn[kCntMergeLoad] += ca + cb;
-                }
-#pragma unroll
-                for (int c = 0; c < kCntProbe; c++) {
-                    const uint32_t t = __reduce_add_sync(kFull, cn[c]);
-                    if (lane == 0 && t) atomicAdd(cnt + c, static_cast<unsigned long long>(t));
-                }
-            }
-            ia += __shfl_sync(kFull, i, 31);
-            ib += __shfl_sync(kFull, j, 31);
-            d += dc;
-        }
     }
     // U hash-form probes per lane, stage by stage so the U chains' loads overlap:
     // list element + its edge id (coalesced) -> first table slot -> (collisions) ->
@@ -620,7 +495,7 @@ __device__ void phase_prep(const DevGraph& g, const uint32_t* curr, uint32_t cs,
     prep_items<kPeelThreads>(cs, [&](uint32_t t) {
         const ITask k = ptask(g, curr[t]);
         desc[t] = make_uint4(k.oa, k.la, k.ob, k.lb);
-        return task_work(k);
+        return k.la;
     }, wpre, bsum);
 }
 
@@ -645,9 +520,7 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             unsigned long long* cnt, uint32_t B, uint32_t* X, uint32_t* xcnt,
                                             const uint32_t* pbits, const uint4* desc) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
-    __shared__ uint32_t smerge[TDG_MERGE_RATIO ? kWarps * 2 * kMergeC : 1];
-    PeelPolicy<kCount> P{g, ss, level, K, curr, ph, next, g.adj, cnt, B, X, xcnt, pbits, desc,
-                         smerge + (TDG_MERGE_RATIO ? (threadIdx.x >> 5) * 2 * kMergeC : 0)};
+    PeelPolicy<kCount> P{g, ss, level, K, curr, ph, next, g.adj, cnt, B, X, xcnt, pbits, desc};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }
 
@@ -831,10 +704,39 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
 
+// Grid-wide barrier of the persistent kernel. TDG_FAST_BARRIER: one fire-and-forget
+// red.release per block on a monotone arrival counter and an ld.acquire spin of thread 0
+// (no returned atomic on the critical path); else cooperative_groups' grid.sync().
+#ifndef TDG_FAST_BARRIER
+#define TDG_FAST_BARRIER 0
+#endif
+struct GridBar {
+    cg::grid_group grid;
+    uint32_t* ctr;
+    uint32_t target;
+    __device__ __forceinline__ void sync() {
+        if (TDG_FAST_BARRIER) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                target += gridDim.x;
+                __threadfence();
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+                uint32_t v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                } while (static_cast<int>(v - target) < 0);
+            }
+            __syncthreads();
+        } else {
+            grid.sync();
+        }
+    }
+};
+
 // The whole truss_parallel level loop (truss_parallel.cpp:119-144) in one launch.
 template <bool kCount>
 __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g, PeelBufs pb) {
-    cg::grid_group grid = cg::this_grid();
+    GridBar grid{cg::this_grid(), &pb.ctl->bar, 0u};
     PeelCtl* ctl = pb.ctl;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m;

@@ -117,12 +117,14 @@ struct SupportPolicy {
 // are too small to pay for the table, or whose owner list exceeds the table, are batched
 // and searched in global memory as before.
 #ifndef TDG_SUP_TAB
-#define TDG_SUP_TAB 4096  // shared-memory table slots (8 B each): owners with d+ <= 3/4 TAB
+#define TDG_SUP_TAB 4096  // shared-memory table slots (4 B key + 2 B position): owners with d+ <= 3/4 TAB
 #endif
 constexpr uint32_t kSupTab = TDG_SUP_TAB;
 #ifndef TDG_SUP_LOAD
-#define TDG_SUP_LOAD 4  // table slots per key when the table is not full size (most probes miss)
+#define TDG_SUP_LOAD 2  // table slots per key when the table is not full size
 #endif
+constexpr size_t kSupSmem = size_t(kSupTab) * (sizeof(uint32_t) + sizeof(uint16_t));
+static_assert(kSupTab % 4 == 0 && 3 * kSupTab / 4 < 65536, "bucketed owner table: u16 positions");
 #ifndef TDG_SUP_SEGMIN
 #define TDG_SUP_SEGMIN 512u  // a segment gets a table if its probes * SEGDIV >= max(d+(x), SEGMIN)
 #endif
@@ -141,22 +143,30 @@ __device__ __forceinline__ uint32_t tab_hash(uint32_t c, uint32_t mask) {
     return (c * 0x9E3779B1u) >> (__clz(mask) & 31u);
 }
 
+// Owner table in shared memory, BUCKETED: 4-key buckets (one 16-byte LDS.128 compares four
+// keys), linear probing over buckets, keys claimed in slot order inside a bucket (so a
+// bucket whose last slot is empty ends a miss); the position of the key in N+(x) sits in a
+// parallel u16 array, read only on a hit. (The previous 8-byte (key, position) slots with
+// per-slot probing took ~3-8 dependent shared loads per miss at the 3/4 load of the
+// d+ > 1024 owners that carry ~70 % of C5's probes.)
 struct SupportTabPolicy {
     const DevGraph& g;
     uint32_t* s;
     const uint32_t* elems;
-    const uint2* tab;
-    uint32_t mask;
+    const uint4* keys4;      // nb buckets of 4 keys
+    const uint16_t* pos;     // 4 * nb positions
+    uint32_t bmask;          // nb - 1
     static constexpr bool kFast = true;
     static constexpr int kUnroll = TDG_SUP_U;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ uint32_t find(const ITask&, uint32_t c) const {
-        uint32_t h = tab_hash(c, mask);
+        uint32_t b = tab_hash(c, bmask);
         while (true) {
-            const uint2 e = tab[h];
-            if (e.x == c) return e.y;
-            if (e.x == kHEmpty) return kNone;
-            h = (h + 1) & mask;
+            const uint4 v = keys4[b];
+            const uint32_t k = v.x == c ? 0u : v.y == c ? 1u : v.z == c ? 2u : v.w == c ? 3u : 4u;
+            if (k < 4u) return pos[4u * b + k];
+            if (v.w == kHEmpty) return kNone;
+            b = (b + 1) & bmask;
         }
     }
     // U items per lane per engine step: the U list loads and lookups issue together and
@@ -186,7 +196,7 @@ __device__ __forceinline__ uint32_t task_in(unsigned long long x, uint32_t lo, u
 __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
                                                           const unsigned long long* wpre, const unsigned long long* bsum,
                                                           uint32_t nchunks, SupportCtl* ctl) {
-    extern __shared__ uint2 tab[];
+    extern __shared__ uint4 tab_keys4[];  // kSupTab keys, then kSupTab u16 positions
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     __shared__ uint32_t sh_p;
     const unsigned long long W = chunk_offsets<kThreads>(bsum, nchunks, sboff);
@@ -235,7 +245,11 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
             // table segment: owner x, tasks [j, tend), items [bend, send)
             uint32_t size = 64;
             while (size < TDG_SUP_LOAD * dp && size < kSupTab) size <<= 1;  // load <= 1/LOAD, or <= 3/4 at full size
-            for (uint32_t q = threadIdx.x; q < size; q += kThreads) tab[q] = make_uint2(kHEmpty, 0u);
+            uint32_t* keys = reinterpret_cast<uint32_t*>(tab_keys4);
+            uint16_t* tpos = reinterpret_cast<uint16_t*>(keys + kSupTab);
+            const uint32_t bmask = size / 4 - 1;
+            for (uint32_t q = threadIdx.x; q < size / 4; q += kThreads)
+                tab_keys4[q] = make_uint4(kHEmpty, kHEmpty, kHEmpty, kHEmpty);
             if (threadIdx.x == 0) {
                 atomicAdd(&ctl->tab_elems, static_cast<unsigned long long>(dp));
                 atomicAdd(&ctl->tab_segments, 1ull);
@@ -244,12 +258,19 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
             const uint32_t o = g.opos[x];
             for (uint32_t q = threadIdx.x; q < dp; q += kThreads) {
                 const uint32_t c = g.oadj[o + q];
-                uint32_t h = tab_hash(c, size - 1);
-                while (atomicCAS(&tab[h].x, kHEmpty, c) != kHEmpty) h = (h + 1) & (size - 1);
-                tab[h].y = q;  // position in N+(x), as the search form's find returns
+                uint32_t b = tab_hash(c, bmask);
+                while (true) {  // first free slot of the bucket (slots fill in order), else the next bucket
+                    uint32_t k = 0;
+                    while (k < 4u && atomicCAS(&keys[4u * b + k], kHEmpty, c) != kHEmpty) k++;
+                    if (k < 4u) {
+                        tpos[4u * b + k] = static_cast<uint16_t>(q);  // position in N+(x), as the search form's find returns
+                        break;
+                    }
+                    b = (b + 1) & bmask;
+                }
             }
             __syncthreads();
-            SupportTabPolicy TP{g, s, g.oadj, tab, size - 1};
+            SupportTabPolicy TP{g, s, g.oadj, tab_keys4, tpos, bmask};
             const unsigned long long w0 = bend + (send - bend) * wid / kSupWarps;
             const unsigned long long w1 = bend + (send - bend) * (wid + 1) / kSupWarps;
             if (w0 < w1) run_items(TP, w0, w1, task_in(w0, j, tend, wpre, sboff, CH), m, wpre, sboff, CH);
@@ -342,7 +363,7 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* w
         return !(e && e[0] == 's');
     }();
     if (tab_form) {
-        const size_t smem = size_t(kSupTab) * sizeof(uint2);
+        const size_t smem = kSupSmem;
         // per-device attribute: set on every call (contexts may sit on different devices)
         err = cudaFuncSetAttribute(k_support_tab, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (err != cudaSuccess) return err;

@@ -166,8 +166,6 @@ enum PeelCnt : int {
     kCntRepair,      // repairs (+1 after a decrement at or below the level)
     kCntNext,        // next-frontier appends (+ stamp stores)
     kCntCross,       // crosser appends
-    kCntMerge,       // merge-task diagonal steps (also part of the probe total W)
-    kCntMergeLoad,   // merge-task list elements staged into shared memory
     kCntProbe,       // ---- below: per-entry compaction tallies (count mode)
     kCntCompIn = kCntProbe,  // compaction: list entries read (adj + eid + processed bit)
     kCntCompKept,    // compaction: entries written back
@@ -199,7 +197,7 @@ struct PeelCtl {
     unsigned long long cnt[kPeelCnt];  // access tallies (PeelCnt); probe-level ones only in count mode
     uint32_t xcnt[2];  // crosser-list append counters (peel.cu near/far scan)
     uint32_t rebuilds;  // scans that re-split the far list
-    uint32_t pad2;
+    uint32_t bar;       // grid-barrier arrival counter (TDG_FAST_BARRIER)
 };
 struct PeelBufs {
     uint32_t* s;               // support (u32): input of the peel / step-function I/O

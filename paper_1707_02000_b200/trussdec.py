@@ -211,7 +211,7 @@ class Context:
             pass
 
     COUNTER_NAMES = ("filter", "pbits", "walk", "slots", "hits", "dead", "dec", "repair", "next", "cross",
-                     "merge", "merge_load", "comp_in", "comp_kept", "comp_long", "scan_in", "scan_out", "tasks", "sorted", "marks",
+                     "comp_in", "comp_kept", "comp_long", "scan_in", "scan_out", "tasks", "sorted", "marks",
                      "sup_tab_elems", "sup_segments", "sup_search")
 
     def counters(self) -> dict:

@@ -23,7 +23,8 @@ for f in sorted(glob.glob(os.path.join(src, "ncu_traffic_C*.csv"))):
     for r in body:
         if len(r) < len(hdr):
             continue
-        name = r[ix["Kernel Name"]].split("<")[0].split("(")[0]
+        mk = re.search(r"(k_[a-z_0-9]+)", r[ix["Kernel Name"]])
+        name = mk.group(1) if mk else r[ix["Kernel Name"]]
         key = (r[ix["ID"]], name)
         v = r[ix["Metric Value"]].replace(",", "")
         try:
@@ -33,7 +34,8 @@ for f in sorted(glob.glob(os.path.join(src, "ncu_traffic_C*.csv"))):
         unit = r[ix["Metric Unit"]]
         mname = r[ix["Metric Name"]]
         if mname == "gpu__time_duration.sum":
-            v = v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1.0)
+            v = v * {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0,
+                     "s": 1e3, "second": 1e3}.get(unit, 1.0)
         if mname.startswith("dram__bytes"):
             v = v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
         per.setdefault(key, {})[mname] = v

@@ -62,3 +62,13 @@ def test_version_and_error_without_gpu():
     g = trussdec.CsrGraph.from_arrays(np.array([0, 1, 2], np.int64), np.array([1, 0], np.int32))
     with pytest.raises(RuntimeError):
         trussdec.truss_parallel(g)
+
+
+def test_counter_names_follow_the_header():
+    """tdg_counters: the Python names list the header's TDG_CNT_* enum in order."""
+    from paper_1707_02000_b200 import trussdec
+    txt = open(os.path.join(ROOT, "include", "tdg.h")).read()
+    i0 = txt.index("TDG_CNT_FILTER = 0")
+    body = txt[i0: txt.index("TDG_NCOUNTERS", i0)]
+    names = [n.lower() for n in re.findall(r"TDG_CNT_([A-Z_]+)", body)]
+    assert names == list(trussdec.Context.COUNTER_NAMES)
