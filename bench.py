@@ -140,9 +140,10 @@ def peel_bytes(c: dict, n: int, m: int, probes: int) -> dict:
     full 32 B sector, no L2 reuse — an upper bound). Returns {"elem": {...}, "sector": {...}}."""
     g = lambda k: int(c.get(k, 0))  # noqa: E731
     elem = {
-        # probe: list element + edge id (coalesced), filter word, processed-bitmap word, table
-        # slots, two edge-state words per hit, atomics as read+write, appends (+ stamp store)
-        "process": 8 * probes + 8 * g("filter") + 4 * g("pbits") + 8 * g("slots") + 16 * g("hits")
+        # probe: list element + edge id (coalesced), filter word, processed-bitmap word, one
+        # 16 B key vector per table bucket read, the 4 B value and two edge-state words per
+        # hit, atomics as read + write, appends (+ stamp store)
+        "process": 8 * probes + 8 * g("filter") + 4 * g("pbits") + 16 * g("slots") + 20 * g("hits")
                    + 8 * g("dec") + 8 * g("repair") + 8 * g("next") + 4 * g("cross"),
         # per task: curr + el + 2 dl + off(a) + off(b), off(b+1) read, descriptor + work prefix written and
         # re-read by the process phase
@@ -156,7 +157,7 @@ def peel_bytes(c: dict, n: int, m: int, probes: int) -> dict:
         "init": 12 * m + 4 * n,
     }
     sec = {
-        "process": 8 * probes + 32 * g("filter") + 32 * g("pbits") + 32 * g("walk") + 8 * (g("slots") - g("walk"))
+        "process": 8 * probes + 32 * g("filter") + 32 * g("pbits") + 32 * g("slots")
                    + 64 * g("hits") + 32 * g("dec") + 4 * g("next") + 4 * g("cross"),
         "prep": 216 * g("tasks"),
         "sort": 204 * g("sorted"),

@@ -115,46 +115,49 @@ __global__ void k_opos(const uint32_t* __restrict__ off, const uint32_t* __restr
     if (u <= n) opos[u] = pos[off[u]];
 }
 
-__device__ __forceinline__ unsigned long long htab_entry(const uint32_t* __restrict__ off, uint32_t x, uint32_t y,
-                                                         uint32_t e) {
+// Value stored with neighbour y in x's table: edge id | (y after x in the (degree, id) order).
+__device__ __forceinline__ uint32_t htab_value(const uint32_t* __restrict__ off, uint32_t x, uint32_t y, uint32_t e) {
     const uint32_t dx = off[x + 1] - off[x], dy = off[y + 1] - off[y];
     const bool up = dx < dy || (dx == dy && x < y);
-    return (static_cast<unsigned long long>(e | (up ? kHUp : 0u)) << 32) | y;
+    return e | (up ? kHUp : 0u);
 }
 
-// Tables of at most kHSmall slots are built in shared memory, one warp per vertex (up to kHMid,
-// one block per vertex), and written out with coalesced stores (random global CAS inserts were
-// 1.8 % of a C5 step). Table of x: kHF * d(x) slots at slot kHF * off[x] (tdg_common.cuh).
-constexpr uint32_t kHSmall = 1024;
+// Buckets per vertex: hq[x] = nb(x) (hq[n] = 0), scanned into the bucket offsets hbo.
+__global__ void k_hsize(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ hq) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) hq[u] = hbuckets(off[u + 1] - off[u]);
+    else if (u == n) hq[n] = 0;
+}
+
+// Tables of at most kHSmall buckets are built in shared memory, one warp per vertex (up to
+// kHMid, one block per vertex), and written out with coalesced stores (random global CAS
+// inserts were 1.8 % of a C5 step).
+constexpr uint32_t kHSmall = 256;        // buckets (8 KB) per warp
 constexpr uint32_t kHMid = 8 * kHSmall;  // block-built tables use the block's whole 64 KB
 
-__device__ __forceinline__ void hinsert_smem(unsigned long long* t, uint32_t T, uint32_t y, unsigned long long entry) {
-    uint32_t h = hslot(hmix(y), T);
-    while (atomicCAS(&t[h], ~0ull, entry) != ~0ull) h = hnext(h, T);
-}
-
 __global__ void __launch_bounds__(256) k_hbuild_small(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                                                      const uint32_t* __restrict__ eid, uint32_t n,
-                                                      unsigned long long* __restrict__ htab) {
-    extern __shared__ unsigned long long htab_smem[];  // 8 warps x kHSmall slots
+                                                      const uint32_t* __restrict__ eid, const uint32_t* __restrict__ hbo,
+                                                      uint32_t n, uint32_t* __restrict__ htab) {
+    extern __shared__ uint32_t htab_smem[];  // 8 warps x kHSmall buckets x 8 words
     const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    unsigned long long* t = htab_smem + w * kHSmall;
+    uint32_t* t = htab_smem + w * kHSmall * 8u;
     for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < n; x += (gridDim.x * blockDim.x) >> 5) {
-        const uint32_t o = off[x], d = off[x + 1] - o, T = kHF * d;
-        if (T == 0 || T > kHSmall) continue;
-        for (uint32_t i = lane; i < T; i += 32) t[i] = ~0ull;
+        const uint32_t b0 = hbo[x], nb = hbo[x + 1] - b0;
+        if (nb == 0 || nb > kHSmall) continue;
+        for (uint32_t i = lane; i < 8u * nb; i += 32) t[i] = kHEmpty;
         __syncwarp();
+        const uint32_t o = off[x], d = off[x + 1] - o;
         for (uint32_t i = lane; i < d; i += 32) {
             const uint32_t y = adj[o + i];
-            hinsert_smem(t, T, y, htab_entry(off, x, y, eid[o + i]));
+            bucket_insert(t, nb, y, htab_value(off, x, y, eid[o + i]));
         }
         __syncwarp();
-        unsigned long long* g = htab + uint64_t(kHF) * o;
-        for (uint32_t i = lane; i < T; i += 32) g[i] = t[i];
+        uint32_t* g = htab + 8ull * b0;
+        for (uint32_t i = lane; i < 8u * nb; i += 32) g[i] = t[i];
         __syncwarp();
     }
-    // Tables of kHSmall < T <= kHMid slots: the whole block builds one at a time in the same
-    // shared memory. Each block takes 256-vertex chunks and queues their mid-size tables.
+    // Tables of kHSmall < nb <= kHMid buckets: the whole block builds one at a time in the
+    // same shared memory. Each block takes 256-vertex chunks and queues their mid-size tables.
     __shared__ uint32_t q[256];
     __shared__ uint32_t qn;
     for (uint64_t c0 = uint64_t(blockIdx.x) * 256; c0 < n; c0 += uint64_t(gridDim.x) * 256) {
@@ -162,53 +165,51 @@ __global__ void __launch_bounds__(256) k_hbuild_small(const uint32_t* __restrict
         __syncthreads();
         const uint64_t x = c0 + threadIdx.x;
         if (x < n) {
-            const uint32_t T = kHF * (off[x + 1] - off[x]);
-            if (T > kHSmall && T <= kHMid) q[atomicAdd(&qn, 1u)] = static_cast<uint32_t>(x);
+            const uint32_t nb = hbo[x + 1] - hbo[x];
+            if (nb > kHSmall && nb <= kHMid) q[atomicAdd(&qn, 1u)] = static_cast<uint32_t>(x);
         }
         __syncthreads();
         const uint32_t cnt = qn;
         for (uint32_t k = 0; k < cnt; k++) {
-            const uint32_t v = q[k], o = off[v], d = off[v + 1] - o, T = kHF * d;
-            for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) htab_smem[i] = ~0ull;
+            const uint32_t v = q[k], b0 = hbo[v], nb = hbo[v + 1] - b0, o = off[v], d = off[v + 1] - o;
+            for (uint32_t i = threadIdx.x; i < 8u * nb; i += blockDim.x) htab_smem[i] = kHEmpty;
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
                 const uint32_t y = adj[o + i];
-                hinsert_smem(htab_smem, T, y, htab_entry(off, v, y, eid[o + i]));
+                bucket_insert(htab_smem, nb, y, htab_value(off, v, y, eid[o + i]));
             }
             __syncthreads();
-            unsigned long long* g = htab + uint64_t(kHF) * o;
-            for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) g[i] = htab_smem[i];
+            uint32_t* g = htab + 8ull * b0;
+            for (uint32_t i = threadIdx.x; i < 8u * nb; i += blockDim.x) g[i] = htab_smem[i];
             __syncthreads();
         }
     }
 }
 
-// Insert every slot (x -> y, eid) of a big table into x's table; the value carries the
-// orientation bit.
+// Insert every slot (x -> y, eid) of a big table (> kHMid buckets) into x's table in global memory.
 __global__ void k_hinsert(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                          const uint32_t* __restrict__ src, const uint32_t* __restrict__ eid, uint64_t slots,
-                          unsigned long long* __restrict__ htab) {
+                          const uint32_t* __restrict__ src, const uint32_t* __restrict__ eid,
+                          const uint32_t* __restrict__ hbo, uint64_t slots, uint32_t* __restrict__ htab) {
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t x = src[j], y = adj[j];
-        const uint32_t o = off[x], T = kHF * (off[x + 1] - o);
-        if (T <= kHMid) continue;
-        unsigned long long* tab = htab + uint64_t(kHF) * o;
-        const unsigned long long entry = htab_entry(off, x, y, eid[j]);
-        uint32_t h = hslot(hmix(y), T);
-        while (atomicCAS(&tab[h], ~0ull, entry) != ~0ull) h = hnext(h, T);
+        const uint32_t x = src[j];
+        const uint32_t b0 = hbo[x], nb = hbo[x + 1] - b0;
+        if (nb <= kHMid) continue;
+        const uint32_t y = adj[j];
+        bucket_insert(htab + 8ull * b0, nb, y, htab_value(off, x, y, eid[j]));
     }
 }
 
 // Filter bits of every slot (x -> y) whose owner table is big enough (tdg_common.cuh).
-__global__ void k_finsert(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
+__global__ void k_finsert(const uint32_t* __restrict__ hbo, const uint32_t* __restrict__ adj,
                           const uint32_t* __restrict__ src, uint64_t slots, unsigned long long* __restrict__ filt) {
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t x = src[j], y = adj[j];
-        const uint32_t o = off[x], d = off[x + 1] - o;
-        if (kHF * d < kFMin) continue;
-        atomicOr(&filt[fword_index(o, d, y)], fbits(hmix(y)));
+        const uint32_t x = src[j];
+        const uint32_t b0 = hbo[x], nb = hbo[x + 1] - b0;
+        if (nb < kFMin) continue;
+        const uint32_t y = adj[j];
+        atomicOr(&filt[fword_index(b0, nb, y)], fbits(hmix(y)));
     }
 }
 
@@ -391,31 +392,35 @@ cudaError_t launch_to_ref(const uint32_t* oeid, const uint32_t* in, uint32_t m, 
 }
 
 cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, const uint32_t* eid,
-                             uint32_t n, uint32_t m, unsigned long long* htab, cudaStream_t st, uint32_t* launches) {
-    if (m == 0) return cudaSuccess;
+                             uint32_t n, uint32_t m, uint32_t* hq, uint32_t* hbo, uint32_t* htab, void* cub_tmp,
+                             size_t cub_bytes, cudaStream_t st, uint32_t* launches) {
+    k_hsize<<<grid_for(uint64_t(n) + 1), kThreads, 0, st>>>(off, n, hq);
+    (*launches)++;
+    size_t tmp = cub_bytes;
+    cudaError_t err = cub::DeviceScan::ExclusiveSum(cub_tmp, tmp, hq, hbo, static_cast<uint64_t>(n) + 1, st);
+    if (err != cudaSuccess || m == 0) return err;
     const uint64_t slots = 2ull * m;
-    cudaError_t err = cudaMemsetAsync(htab, 0xff, htab_slots(m) * sizeof(unsigned long long), st);
-    if (err != cudaSuccess) return err;
+    if ((err = cudaMemsetAsync(htab, 0xff, htab_buckets(n, m) * 32, st)) != cudaSuccess) return err;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
-    const size_t smem = 8u * kHSmall * sizeof(unsigned long long);
+    const size_t smem = 8u * kHSmall * 8u * sizeof(uint32_t);
     // (a per-function attribute of the CURRENT device: set on every call, contexts may sit on
     // different devices)
     err = cudaFuncSetAttribute(k_hbuild_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (err != cudaSuccess) return err;
-    k_hbuild_small<<<148u * 3u, 256, smem, st>>>(off, adj, eid, n, htab);
-    k_hinsert<<<gs, kThreads, 0, st>>>(off, adj, src, eid, slots, htab);
+    k_hbuild_small<<<148u * 3u, 256, smem, st>>>(off, adj, eid, hbo, n, htab);
+    k_hinsert<<<gs, kThreads, 0, st>>>(off, adj, src, eid, hbo, slots, htab);
     (*launches) += 2;
     return cudaGetLastError();
 }
 
-cudaError_t launch_filter_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, uint32_t m,
+cudaError_t launch_filter_fill(const uint32_t* hbo, const uint32_t* adj, const uint32_t* src, uint32_t n, uint32_t m,
                                unsigned long long* filt, cudaStream_t st, uint32_t* launches) {
     if (m == 0) return cudaSuccess;
-    cudaError_t err = cudaMemsetAsync(filt, 0, filter_words(m) * sizeof(unsigned long long), st);
+    cudaError_t err = cudaMemsetAsync(filt, 0, filter_words(n, m) * sizeof(unsigned long long), st);
     if (err != cudaSuccess) return err;
     const uint64_t slots = 2ull * m;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
-    k_finsert<<<gs, kThreads, 0, st>>>(off, adj, src, slots, filt);
+    k_finsert<<<gs, kThreads, 0, st>>>(hbo, adj, src, slots, filt);
     (*launches)++;
     return cudaGetLastError();
 }

@@ -89,7 +89,7 @@ struct tdg_context {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     // persistent per-graph arrays (live through the peel)
-    DevBuf off64, off, adj, eo, up, P, eid, el, opos, oeid, sbeg, dl, pbits, htab, filt;
+    DevBuf off64, off, adj, eo, up, P, eid, el, opos, oeid, sbeg, dl, pbits, hbo, htab, filt;
     // one arena for the m-sized scratch: the build + support arrays and the peel lists share
     // it (they are never live at the same time; layout in ensure_arena)
     DevBuf arena;
@@ -211,7 +211,8 @@ struct tdg_context {
         g.stask = stask;
         g.sx = sx;
         g.sbeg = sbeg.as<uint32_t>();
-        g.htab = htab.as<unsigned long long>();
+        g.htab = htab.as<uint32_t>();
+        g.hbo = hbo.as<uint32_t>();
         g.filt = peel_filter() ? filt.as<unsigned long long>() : nullptr;
         return g;
     }
@@ -259,7 +260,7 @@ struct tdg_context {
         return p;
     }
     void trim() {
-        DevBuf* all[] = {&off64, &off, &adj, &eo, &up, &P, &eid, &el, &opos, &oeid, &sbeg, &dl, &pbits, &htab, &filt,
+        DevBuf* all[] = {&off64, &off, &adj, &eo, &up, &P, &eid, &el, &opos, &oeid, &sbeg, &dl, &pbits, &hbo, &htab, &filt,
                          &arena, &cchunk, &nsl, &ctl, &sctl, &sacc, &cub, &truss, &sup, &f0, &f1, &f2, &bsum, &bhist,
                          &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1, &kwpre, &kctl, &ktmp, &knoff, &knadj,
                          &kperm, &kbad, &ing, &ptext, &pscr, &ppairs};
@@ -427,13 +428,15 @@ void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, b
     if (internal)  // flag (2m+1 u32) is free once the build is done
         ck(launch_internal_ids(c->build_bufs(off64), d.m, c->flag, c->stream, &c->launches),
            "internal edge ids");
-    if (tables) {  // neighbour -> edge-id hash tables (+ filters): sizes depend on m only
-        c->htab.ensure(htab_slots(d.m) * 8, "hash tables");
+    if (tables) {  // neighbour -> edge-id hash tables (+ filters): sizes depend on n and m only
+        c->hbo.ensure((size_t(d.n) + 1) * 4, "table offsets");
+        c->htab.ensure(htab_buckets(d.n, d.m) * 32, "hash tables");
         ck(launch_htab_fill(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->src, c->eid.as<uint32_t>(), d.n, d.m,
-                            c->htab.as<unsigned long long>(), c->stream, &c->launches), "hash fill");
+                            c->up.as<uint32_t>(), c->hbo.as<uint32_t>(), c->htab.as<uint32_t>(), c->cub.p, c->cub.cap,
+                            c->stream, &c->launches), "hash fill");
         if (peel_filter()) {
-            c->filt.ensure(filter_words(d.m) * 8, "filters");
-            ck(launch_filter_fill(c->off.as<uint32_t>(), c->adj.as<uint32_t>(), c->src, d.m,
+            c->filt.ensure(filter_words(d.n, d.m) * 8, "filters");
+            ck(launch_filter_fill(c->hbo.as<uint32_t>(), c->adj.as<uint32_t>(), c->src, d.n, d.m,
                                   c->filt.as<unsigned long long>(), c->stream, &c->launches), "filter fill");
         }
     }

@@ -61,15 +61,13 @@ constexpr int kScanItems = 8;
 constexpr int kWarps = kPeelThreads / 32;
 
 // Task of e1 = (u,v): probe the shorter live list a against the other endpoint b's
-// neighbour -> edge-id hash table (ob = off[b], lb = d(b): the table is kHF * d(b) slots at
-// slot kHF * off[b], tdg_common.cuh).
+// neighbour -> edge-id hash table (ob = hbo[b], lb = its bucket count, tdg_common.cuh).
 #ifndef TDG_HTAB_NC
 #define TDG_HTAB_NC 0  // table slots through the read-only (non-coherent) path: tables never change in the peel
 #endif
 #ifndef TDG_PEEL_FAST
 #define TDG_PEEL_FAST 0  // engine fast path (intersect.cuh) for the peel's probe loop
 #endif
-// ob = off[b], lb = d(b) (b's table: kHF * d(b) slots at slot kHF * off[b]).
 __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
     const uint2 p = g.el[e1];
     const uint32_t du = g.dl[p.x], dv = g.dl[p.y];
@@ -80,8 +78,8 @@ __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
     k.oa = g.off[a];
     k.la = pu ? du : dv;
     k.aux = b;
-    k.ob = g.off[b];
-    k.lb = g.off[b + 1] - k.ob;
+    k.ob = g.hbo[b];
+    k.lb = g.hbo[b + 1] - k.ob;
     return k;
 }
 
@@ -227,7 +225,6 @@ struct PeelPolicy {
     template <int U>
     __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
         uint32_t x[U], ea[U], eb[U], h[U];
-        unsigned long long ent[U];
         uint32_t cn[kCntProbe] = {};  // per-lane access tallies (kCount only; folded away otherwise)
 #pragma unroll
         for (int q = 0; q < U; q++) {
@@ -258,7 +255,7 @@ struct PeelPolicy {
 #pragma unroll
             for (int q = 0; q < U; q++) {
                 fw[q] = ~0ull;
-                if (look[q] && kHF * ko[q].lb >= kFMin) {
+                if (look[q] && ko[q].lb >= kFMin) {
                     fw[q] = __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q]));
                     if constexpr (kCount) cn[kCntFilter]++;
                 }
@@ -272,29 +269,36 @@ struct PeelPolicy {
 #pragma unroll
         for (int q = 0; q < U; q++)
             if ((pw[q] >> (ea[q] & 31u)) & 1u) look[q] = false;
-        const unsigned long long* tb[U];  // b's table: kHF * d(b) slots at slot kHF * off[b]
+        // b's table: buckets [ob, ob + lb) of 8 words (4 keys, then their 4 values); one
+        // 16-byte key-vector load per bucket, the value (same sector) only on a hit
+        uint4 kv[U];
+        uint32_t bi[U];
 #pragma unroll
         for (int q = 0; q < U; q++) {
-            ent[q] = kHEmpty;
-            tb[q] = g.htab + uint64_t(kHF) * ko[q].ob;
+            kv[q] = make_uint4(kHEmpty, kHEmpty, kHEmpty, kHEmpty);
+            bi[q] = 0;
             if (look[q]) {
-                h[q] = hslot(h[q], kHF * ko[q].lb);
-                ent[q] = TDG_HTAB_NC ? __ldg(tb[q] + h[q]) : tb[q][h[q]];
+                bi[q] = hbucket(h[q], ko[q].lb);
+                const uint4* kp = reinterpret_cast<const uint4*>(g.htab + 8ull * (ko[q].ob + bi[q]));
+                kv[q] = TDG_HTAB_NC ? __ldg(kp) : *kp;
                 if constexpr (kCount) { cn[kCntWalk]++; cn[kCntSlots]++; }
             }
         }
+        uint32_t sl[U];
 #pragma unroll
         for (int q = 0; q < U; q++) {
-            unsigned long long e = ent[q];
-            uint32_t hh = h[q];
-            while (static_cast<uint32_t>(e) != kHEmpty && static_cast<uint32_t>(e) != x[q]) {
-                hh = hnext(hh, kHF * ko[q].lb);
-                e = TDG_HTAB_NC ? __ldg(tb[q] + hh) : tb[q][hh];
+            sl[q] = bucket_find(kv[q], x[q]);
+            while (sl[q] == 4u && kv[q].w != kHEmpty) {  // home bucket full: the key may sit further on
+                bi[q] = hnext(bi[q], ko[q].lb);
+                const uint4* kp = reinterpret_cast<const uint4*>(g.htab + 8ull * (ko[q].ob + bi[q]));
+                kv[q] = TDG_HTAB_NC ? __ldg(kp) : *kp;
+                sl[q] = bucket_find(kv[q], x[q]);
                 if constexpr (kCount) cn[kCntSlots]++;
             }
-            eb[q] = (x[q] != kHEmpty && static_cast<uint32_t>(e) == x[q]) ? (static_cast<uint32_t>(e >> 32) & ~kHUp)
-                                                                           : kNone;
         }
+#pragma unroll
+        for (int q = 0; q < U; q++)
+            eb[q] = (look[q] && sl[q] < 4u) ? (g.htab[8ull * (ko[q].ob + bi[q]) + 4u + sl[q]] & ~kHUp) : kNone;
         uint32_t ids[U];
 #pragma unroll
         for (int q = 0; q < U; q++) ids[q] = ko[q].id;

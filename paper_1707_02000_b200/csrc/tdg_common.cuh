@@ -119,13 +119,15 @@ __device__ __forceinline__ uint32_t warp_append(bool pred, uint32_t* counter) {
 }
 
 // ---- per-vertex neighbour -> edge-id hash tables (built once per graph, never compacted)
-// Table of x: kHF * d(x) slots at slot offset kHF * off[x] (load factor exactly 1/kHF; the
-// layout is a pure function of the CSR offsets, so the total kHF * 2m is known before the
-// build — no size readback). Linear probing from slot hslot(hmix(key), T), wrapping at T.
-// Entry = (value << 32) | key, key = neighbour id (kHEmpty = free slot),
-// value = edge id | (neighbour after x in the (degree, id) order ? 1<<31 : 0).
+// BUCKETED: the table of x is nb(x) = ceil(kHF * d(x) / 4) buckets of 32 bytes (one DRAM
+// sector) at bucket offset hbo[x] (exclusive scan of nb; the total is bounded by
+// kHF * 2m / 4 + n, known before the build — no size readback). A bucket holds 4 keys
+// (neighbour ids, kHEmpty = free) then their 4 values (edge id | (neighbour after x in the
+// (degree, id) order ? kHUp : 0)). A key lives in its home bucket hbucket(hmix(key), nb) or,
+// if that is full, in the following ones (linear probing over buckets); slots fill in order,
+// so a lookup reads one 16-byte key vector per bucket and stops at a bucket with a free slot.
 #ifndef TDG_HT_FACTOR
-#define TDG_HT_FACTOR 2  // table slots per neighbour (C5: 2 -> 32 B per edge of tables)
+#define TDG_HT_FACTOR 2  // table slots per neighbour (load factor 1/kHF): C5 tables 32 B per edge
 #endif
 constexpr uint32_t kHF = TDG_HT_FACTOR;
 constexpr uint32_t kHEmpty = 0xffffffffu;
@@ -139,28 +141,46 @@ __device__ __forceinline__ uint32_t hmix(uint32_t x) {
     x ^= x >> 16;
     return x;
 }
-// First slot of hash h in a table of T slots (multiply-high range reduction, any T).
-__device__ __forceinline__ uint32_t hslot(uint32_t h, uint32_t T) { return __umulhi(h, T); }
-__device__ __forceinline__ uint32_t hnext(uint32_t i, uint32_t T) { return i + 1 == T ? 0u : i + 1; }
+__host__ __device__ __forceinline__ uint32_t hbuckets(uint32_t d) { return (kHF * d + 3u) / 4u; }
+// Home bucket of hash h in a table of nb buckets (multiply-high range reduction, any nb).
+__device__ __forceinline__ uint32_t hbucket(uint32_t h, uint32_t nb) { return __umulhi(h, nb); }
+__device__ __forceinline__ uint32_t hnext(uint32_t i, uint32_t nb) { return i + 1 == nb ? 0u : i + 1; }
+// Slot (0..3) of key x in a bucket's key vector, 4 if absent.
+__device__ __forceinline__ uint32_t bucket_find(const uint4& k, uint32_t x) {
+    return k.x == x ? 0u : k.y == x ? 1u : k.z == x ? 2u : k.w == x ? 3u : 4u;
+}
+// Insert (key y, value v) into the bucketed table t of nb buckets (global or shared memory).
+__device__ __forceinline__ void bucket_insert(uint32_t* t, uint32_t nb, uint32_t y, uint32_t v) {
+    uint32_t b = hbucket(hmix(y), nb);
+    while (true) {
+        uint32_t k = 0;
+        while (k < 4u && atomicCAS(&t[8u * b + k], kHEmpty, y) != kHEmpty) k++;
+        if (k < 4u) {
+            t[8u * b + 4u + k] = v;
+            return;
+        }
+        b = hnext(b, nb);
+    }
+}
 
 // ---- per-vertex membership filters (register-blocked Bloom filters) in front of the big
-// tables (T >= kFMin slots). Vertex x owns the 64-bit words [off[x] >> kFShift,
-// off[x+1] >> kFShift) — disjoint ranges, 2^kFShift adjacency slots per word, i.e.
-// 64 / 2^kFShift bits per key. A key sets TDG_FK bits of one word; a lookup whose bits are
-// not all set is a certain miss and skips the table walk, so the misses of a sub-level
-// (~3/4 of all probes) mostly hit the L2-resident filters instead of DRAM.
+// tables (nb >= kFMin buckets). Vertex x owns the 64-bit words [hbo[x] >> kFShift,
+// hbo[x+1] >> kFShift) — disjoint ranges, 2^kFShift buckets (~2^(kFShift+2) / kHF keys) per
+// word: 4 bits per key at kHF = 2, kFShift = 3. A key sets TDG_FK bits of one word; a lookup
+// whose bits are not all set is a certain miss and skips the table walk, so the misses of a
+// sub-level (~3/4 of all probes) mostly hit the L2-resident filters instead of DRAM.
 #ifndef TDG_FMIN
-#define TDG_FMIN 1024
+#define TDG_FMIN 256  // buckets (1024 slots)
 #endif
 constexpr uint32_t kFMin = TDG_FMIN;
 #ifndef TDG_FSHIFT
-#define TDG_FSHIFT 4  // 4 bits per key: sparser filters stay L2-resident (C5: 16 -> 8 -> 4 bits, 3.47 -> 3.26 -> 3.19 s)
+#define TDG_FSHIFT 3  // 4 bits per key: sparser filters stay L2-resident (C5: 16 -> 8 -> 4 bits, 3.47 -> 3.26 -> 3.19 s)
 #endif
 #ifndef TDG_FK
 #define TDG_FK 3  // bits set per key
 #endif
 constexpr uint32_t kFShift = TDG_FSHIFT;
-static_assert((kFMin / kHF) >> kFShift >= 1, "every filtered vertex owns at least one filter word");
+static_assert((kFMin >> kFShift) >= 1, "every filtered vertex owns at least one filter word");
 
 __device__ __forceinline__ uint32_t fword(uint32_t x) {
     x = (x ^ 0x9e3779b9u) * 0x85ebca6bu;
@@ -175,15 +195,16 @@ __device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(k
     return b;
 }
 
-// Filter word of key y in the filter of a vertex whose adjacency is [o, o + d).
-__device__ __forceinline__ uint64_t fword_index(uint32_t o, uint32_t d, uint32_t y) {
-    const uint32_t f0 = o >> kFShift, f1 = (o + d) >> kFShift;
+// Filter word of key y in the filter of a vertex whose table is buckets [ob, ob + nb).
+__device__ __forceinline__ uint64_t fword_index(uint32_t ob, uint32_t nb, uint32_t y) {
+    const uint32_t f0 = ob >> kFShift, f1 = (ob + nb) >> kFShift;
     return static_cast<uint64_t>(f0) + __umulhi(fword(y), f1 - f0);
 }
 
 struct DevGraph {
     uint32_t n = 0, m = 0;
-    const unsigned long long* htab = nullptr;  // hash table slots (kHF * 2m)
+    const uint32_t* htab = nullptr;  // bucketed hash tables: 8 u32 words (4 keys, 4 values) per bucket
+    const uint32_t* hbo = nullptr;   // n+1 bucket offsets
     const unsigned long long* filt = nullptr;  // membership filters of the big tables (or null)
     const uint32_t* off = nullptr;
     uint32_t* adj = nullptr;

@@ -44,14 +44,15 @@ cudaError_t launch_internal_ids(const BuildBufs& b, uint32_t m, uint32_t* r2i, c
 cudaError_t launch_to_ref(const uint32_t* oeid, const uint32_t* in, uint32_t m, uint32_t add, uint32_t* out,
                           cudaStream_t st, uint32_t* launches);
 
-// Per-vertex neighbour -> edge-id hash tables (tdg_common.cuh): kHF * 2m slots of 8 bytes,
-// and the membership filters of the big tables: filter_words(m) 64-bit words. Both sizes
-// depend on m only (no readback between build steps).
-inline uint64_t htab_slots(uint64_t m) { return uint64_t(kHF) * 2 * m; }
-inline uint64_t filter_words(uint64_t m) { return ((2 * m) >> kFShift) + 1; }
+// Per-vertex neighbour -> edge-id hash tables (tdg_common.cuh): bucket offsets hbo[n+1]
+// (hq: n+1 scratch) and at most htab_buckets(n, m) buckets of 32 bytes; the membership filters
+// of the big tables: filter_words(n, m) 64-bit words. All sizes follow from n and m.
+inline uint64_t htab_buckets(uint64_t n, uint64_t m) { return (uint64_t(kHF) * 2 * m) / 4 + n + 1; }
+inline uint64_t filter_words(uint64_t n, uint64_t m) { return (htab_buckets(n, m) >> kFShift) + 1; }
 cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, const uint32_t* eid,
-                             uint32_t n, uint32_t m, unsigned long long* htab, cudaStream_t st, uint32_t* launches);
-cudaError_t launch_filter_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, uint32_t m,
+                             uint32_t n, uint32_t m, uint32_t* hq, uint32_t* hbo, uint32_t* htab, void* cub_tmp,
+                             size_t cub_bytes, cudaStream_t st, uint32_t* launches);
+cudaError_t launch_filter_fill(const uint32_t* hbo, const uint32_t* adj, const uint32_t* src, uint32_t n, uint32_t m,
                                unsigned long long* filt, cudaStream_t st, uint32_t* launches);
 
 struct StatsAcc {
