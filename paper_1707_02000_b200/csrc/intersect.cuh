@@ -18,21 +18,19 @@
 
 namespace tdg {
 
+// A task as the engine carries it between lanes (its item count lives in the work prefix).
 struct ITask {
     uint32_t id;      // peel: e1 ; support: edge id of the oriented edge a->b
-    uint32_t oa, la;  // probe list
-    uint32_t ob, lb;  // searched vertex: its hash table (quad offset, slot mask)
-    uint32_t aux;     // peel: the searched vertex's id (it never occurs in its own table)
+    uint32_t oa;      // probe list A = elems[oa ..)
+    uint32_t ob, lb;  // searched side (peel: table bucket offset / count; support: N+ list)
 };
 
 __device__ __forceinline__ ITask shfl_task(const ITask& k, uint32_t src) {
     ITask r;
     r.id = __shfl_sync(kFull, k.id, src);
     r.oa = __shfl_sync(kFull, k.oa, src);
-    r.la = __shfl_sync(kFull, k.la, src);
     r.ob = __shfl_sync(kFull, k.ob, src);
     r.lb = __shfl_sync(kFull, k.lb, src);
-    r.aux = __shfl_sync(kFull, k.aux, src);
     return r;
 }
 
@@ -128,10 +126,10 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
     uint32_t i = i0;
     // lanes hold tasks i..i+31 (start st); end_held = start of task i+32
     uint32_t held = kNone;
-    ITask k{0, 0, 0, 0, 0, kNone};
+    ITask k{0, 0, 0, 0};
     unsigned long long st = ~0ull, end_held = ~0ull;
     // fast-path cache: lane 0's task broadcast to every lane, valid while i == c_task
-    ITask c0{0, 0, 0, 0, 0, kNone};
+    ITask c0{0, 0, 0, 0};
     unsigned long long c_st = 0;
     uint32_t c_task = kNone;
     for (unsigned long long base = x0; base < x1;) {
@@ -143,10 +141,8 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
             if (adv < 32) {
                 k.id = __shfl_down_sync(kFull, k.id, adv);
                 k.oa = __shfl_down_sync(kFull, k.oa, adv);
-                k.la = __shfl_down_sync(kFull, k.la, adv);
                 k.ob = __shfl_down_sync(kFull, k.ob, adv);
                 k.lb = __shfl_down_sync(kFull, k.lb, adv);
-                k.aux = __shfl_down_sync(kFull, k.aux, adv);
                 const uint32_t lo = __shfl_down_sync(kFull, static_cast<uint32_t>(st), adv);
                 const uint32_t hi = __shfl_down_sync(kFull, static_cast<uint32_t>(st >> 32), adv);
                 st = (static_cast<unsigned long long>(hi) << 32) | lo;
@@ -234,6 +230,27 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
 #ifndef TDG_PIECES
 #define TDG_PIECES 4ull  // work pieces per warp in process_items (dynamic; smaller = shorter tail)
 #endif
+#ifndef TDG_GUIDED
+#define TDG_GUIDED 1  // guided pieces: tiers of nwarps pieces whose size halves per tier (short tail)
+#endif
+
+// Guided piece schedule over W items for nw warps: tier t holds nw pieces of S0 >> t items
+// (S0 = W / 2nw, whole engine steps), so each tier covers about half of what the previous
+// one left; pieces never shrink below `minp` and the last tier repeats that size. Piece p ->
+// [*x0, *x1) (*x0 >= W: no piece). Dynamic pulling of a piece counter keeps it balanced; the
+// phase tail is one minimum piece instead of one W / (4 nw) piece.
+__device__ __forceinline__ void guided_piece(unsigned long long p, unsigned long long W, uint32_t nw,
+                                             unsigned long long S0, unsigned long long minp,
+                                             unsigned long long* x0, unsigned long long* x1) {
+    unsigned long long base = 0, S = S0 > minp ? S0 : minp;
+    while (S > minp && p >= nw) {
+        base += nw * S;
+        p -= nw;
+        S = (S >> 1) > minp ? (S >> 1) : minp;
+    }
+    *x0 = base + p * S;
+    *x1 = *x0 + S < W ? *x0 + S : W;
+}
 
 // sboff[c] = exclusive prefix of the chunk totals bsum[0..nchunks) (block-wide; smem
 // sboff holds >= nchunks+1 entries); returns the total work.
@@ -266,12 +283,27 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
     if (W == 0) return 0;
     const uint32_t CH = chunk_len(ntasks, nchunks);
     const uint32_t nwarps = (gridDim.x * kThreads) >> 5;
-    unsigned long long PS = (W + TDG_PIECES * nwarps - 1) / (TDG_PIECES * nwarps);
     constexpr unsigned long long kStep = TDG_PIECE_ROUND ? 32ull * Policy::kUnroll : 32ull;
+    const uint32_t lane = lane_id();
+    if (TDG_GUIDED) {
+        unsigned long long S0 = (W + 2ull * nwarps - 1) / (2ull * nwarps);
+        S0 = (S0 + kStep - 1) / kStep * kStep;
+        const unsigned long long minp = kStep > TDG_MIN_PIECE ? kStep : TDG_MIN_PIECE;
+        while (true) {
+            uint32_t p = 0;
+            if (lane == 0) p = atomicAdd(piece_head, 1u);
+            p = __shfl_sync(kFull, p, 0);
+            unsigned long long x0, x1;
+            guided_piece(p, W, nwarps, S0, minp, &x0, &x1);
+            if (x0 >= W) break;
+            run_items(P, x0, x1, task_at(x0, ntasks, wpre, sboff, nchunks, CH), ntasks, wpre, sboff, CH);
+        }
+        return W;
+    }
+    unsigned long long PS = (W + TDG_PIECES * nwarps - 1) / (TDG_PIECES * nwarps);
     PS = (PS + kStep - 1) / kStep * kStep;  // whole engine steps per piece
     if (PS < TDG_MIN_PIECE) PS = TDG_MIN_PIECE;
     const unsigned long long npieces = (W + PS - 1) / PS;
-    const uint32_t lane = lane_id();
 
     while (true) {
         uint32_t p = 0;

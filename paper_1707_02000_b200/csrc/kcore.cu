@@ -57,10 +57,8 @@ struct KcorePolicy {
         ITask k;
         k.id = v;
         k.oa = off[v];
-        k.la = off[v + 1] - k.oa;
         k.ob = 0;
         k.lb = 0;
-        k.aux = kNone;
         return k;
     }
     __device__ uint32_t find(const ITask&, uint32_t w) const { return w; }

@@ -68,7 +68,8 @@ constexpr int kWarps = kPeelThreads / 32;
 #ifndef TDG_PEEL_FAST
 #define TDG_PEEL_FAST 0  // engine fast path (intersect.cuh) for the peel's probe loop
 #endif
-__device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
+// la = the probe count (live length of the shorter list).
+__device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1, uint32_t& la) {
     const uint2 p = g.el[e1];
     const uint32_t du = g.dl[p.x], dv = g.dl[p.y];
     const bool pu = du <= dv;
@@ -76,8 +77,7 @@ __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1) {
     ITask k;
     k.id = e1;
     k.oa = g.off[a];
-    k.la = pu ? du : dv;
-    k.aux = b;
+    la = pu ? du : dv;
     k.ob = g.hbo[b];
     k.lb = g.hbo[b + 1] - k.ob;
     return k;
@@ -156,9 +156,8 @@ struct PeelPolicy {
     static_assert(kUnroll > 1, "the peel's probe loop is the U-chain form (run)");
 
     __device__ ITask load(uint32_t t) const {
-        // (aux = kNone: b's own id never occurs in its table, only a filter miss is lost)
         const uint4 d = desc[t];
-        return ITask{curr[t], d.x, d.y, d.z, d.w, kNone};
+        return ITask{d.x, d.y, d.z, d.w};
     }
     // Triangle visits {e1 = ids[q], ea[q], eb[q]} (eb[q] == kNone: no visit), all lanes together:
     // both peers' state words -> skip on a processed peer (:85) -> ownership + clamp
@@ -239,7 +238,7 @@ struct PeelPolicy {
         bool look[U];
 #pragma unroll
         for (int q = 0; q < U; q++) {
-            look[q] = act[q] && x[q] != ko[q].aux;
+            look[q] = act[q];  // (b itself is in N(a) but never in its own table: a plain miss)
             h[q] = look[q] ? hmix(x[q]) : 0u;
         }
         // ... and so does an own slot already processed in an earlier sub-level (:85): its
@@ -497,9 +496,10 @@ __device__ void phase_bucket_scatter(const DevGraph& g, const uint32_t* curr, ui
 __device__ void phase_prep(const DevGraph& g, const uint32_t* curr, uint32_t cs, unsigned long long* wpre,
                            unsigned long long* bsum, uint4* desc) {
     prep_items<kPeelThreads>(cs, [&](uint32_t t) {
-        const ITask k = ptask(g, curr[t]);
-        desc[t] = make_uint4(k.oa, k.la, k.ob, k.lb);
-        return k.la;
+        uint32_t la;
+        const ITask k = ptask(g, curr[t], la);
+        desc[t] = make_uint4(k.id, k.oa, k.ob, k.lb);
+        return la;
     }, wpre, bsum);
 }
 

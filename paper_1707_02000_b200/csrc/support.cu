@@ -31,9 +31,7 @@ __device__ __forceinline__ ITask otask(const DevGraph& g, uint32_t t) {
     const uint32_t j = g.stask[t], x = g.sx[t], y = g.adj[j];
     ITask k;
     k.id = g.eid[j];
-    k.aux = kNone;
     k.oa = g.opos[y];
-    k.la = g.opos[y + 1] - k.oa;
     k.ob = g.opos[x];
     k.lb = g.opos[x + 1] - k.ob;
     return k;
