@@ -66,8 +66,10 @@ __global__ void k_eid(const uint32_t* __restrict__ off, const uint32_t* __restri
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t u = src[j], v = adj[j];
+        TDG_CHECK(u < (1u << 31) && v != u);
         if (v > u) {
             const uint32_t e = P[u] + static_cast<uint32_t>(j - eo[u]);
+            TDG_CHECK(j >= eo[u]);
             el[e] = make_uint2(u, v);
             eid[j] = e;
             tkey[e] = v;
@@ -90,7 +92,10 @@ __global__ void k_eid_lower(const uint32_t* __restrict__ adj, const uint32_t* __
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t u = src[j];
-        if (adj[j] < u) eid[j] = sorted_ids[j - P[u]];
+        if (adj[j] < u) {
+            TDG_CHECK(j >= P[u] && j - P[u] < slots / 2);
+            eid[j] = sorted_ids[j - P[u]];
+        }
     }
 }
 
@@ -102,6 +107,7 @@ __global__ void k_orient(const uint32_t* __restrict__ adj, const uint32_t* __res
          j += uint64_t(gridDim.x) * blockDim.x) {
         if (!flag[j]) continue;
         const uint32_t t = pos[j], v = adj[j], e = eid[j];
+        TDG_CHECK(t < slots / 2 && e < slots / 2);
         const uint2 p = el[e];
         oadj[t] = v;
         oeid[t] = e;

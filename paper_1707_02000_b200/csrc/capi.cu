@@ -97,8 +97,8 @@ struct tdg_context {
     DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing, ptext, pscr, ppairs;
     // arena views (recomputed by ensure_arena)
     uint32_t *src = nullptr, *flag = nullptr, *pos = nullptr, *oadj = nullptr, *osrc = nullptr, *stask = nullptr,
-             *sx = nullptr, *s = nullptr, *L0 = nullptr, *L1 = nullptr, *Ls = nullptr, *A0 = nullptr, *A1 = nullptr,
-             *F0 = nullptr, *F1 = nullptr, *X0 = nullptr, *X1 = nullptr, *cscr = nullptr;
+             *sx = nullptr, *s = nullptr, *L0 = nullptr, *L1 = nullptr, *A0 = nullptr, *A1 = nullptr, *F0 = nullptr,
+             *F1 = nullptr, *cscr = nullptr;
     unsigned long long *ss = nullptr, *wpre = nullptr;
     size_t word = 0;
     HostCtl* hctl = nullptr;
@@ -107,14 +107,14 @@ struct tdg_context {
 
     void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
 
-    // Arena of 17 "words" of 4(m+1) bytes (256-aligned). Build + support use words
+    // Arena of 14 "words" of 4(m+1) bytes (256-aligned). Build + support use words
     //   2-3 src (-> support work prefix wpre), 4-5 flag (-> internal-id scratch), 6-7 pos,
-    //   8 oadj, 9 osrc, 10 stask, 11 sx, 16 s,
-    // the peel uses 0-1 ss (packed state), 2-3 wpre, 4-7 cscr (task descriptors /
-    // compaction scratch), 8 L0, 9 L1, 10 Ls, 11 A0, 12 A1, 13 F0, 14 F1, 15 X0, 16 X1.
-    // s (16) is read by k_peel_init while it writes ss (0-1); X1 (16) is first written by
-    // the peel's crosser appends, after that.
-    static constexpr int kArenaWords = 17;
+    //   8 oadj, 9 osrc, 10 stask, 11 sx, 12 s,
+    // the peel uses 0-1 ss (packed state), 2-3 wpre, 4-7 cscr (task descriptors + a sorted
+    // curr list / compaction scratch), 8 L0, 9 L1, 10 A0, 11 A1, 12 F0, 13 F1.
+    // s (12) is read by k_peel_init while it writes ss (0-1); F0 (12) is first written by the
+    // peel's first scan, after that.
+    static constexpr int kArenaWords = 14;
     static size_t arena_word(uint64_t m) { return (4 * (m + 1) + 255) & ~size_t(255); }
     void ensure_arena(uint64_t m) {
         word = arena_word(m);
@@ -128,13 +128,10 @@ struct tdg_context {
         pos = w32(6);
         L0 = oadj = w32(8);
         L1 = osrc = w32(9);
-        Ls = stask = w32(10);
-        A0 = sx = w32(11);
-        A1 = w32(12);
-        F0 = w32(13);
-        F1 = w32(14);
-        X0 = w32(15);
-        X1 = s = w32(16);
+        A0 = stask = w32(10);
+        A1 = sx = w32(11);
+        F0 = s = w32(12);
+        F1 = w32(13);
     }
 
     void ensure_graph(uint64_t n, uint64_t m) {
@@ -213,6 +210,7 @@ struct tdg_context {
         g.sbeg = sbeg.as<uint32_t>();
         g.htab = htab.as<uint32_t>();
         g.hbo = hbo.as<uint32_t>();
+        g.nbuckets = htab.cap / 32;
         g.filt = peel_filter() ? filt.as<unsigned long long>() : nullptr;
         return g;
     }
@@ -226,8 +224,6 @@ struct tdg_context {
         p.A[1] = A1;
         p.F[0] = F0;
         p.F[1] = F1;
-        p.X[0] = X0;
-        p.X[1] = X1;
         p.wpre = wpre;
         p.bsum = bsum.as<unsigned long long>();
         p.ctl = ctl.as<PeelCtl>();
@@ -235,7 +231,6 @@ struct tdg_context {
         p.nsl_cap = n + 1;
         const char* ch = std::getenv("TDG_COUNT");
         p.count = (ch && ch[0] == '1') ? 1u : 0u;
-        p.Ls = Ls;
         p.bhist = bhist.as<uint32_t>();
         p.bcur = bcur.as<uint32_t>();
         uint32_t bits = 0;

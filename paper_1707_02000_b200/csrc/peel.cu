@@ -126,6 +126,7 @@ __device__ __forceinline__ void emit_many(const uint32_t (&o)[N], uint32_t* ctr,
     uint32_t base = 0;
     if (lane == 31) base = atomicAdd(ctr, incl);
     base = __shfl_sync(kFull, base, 31) + incl - c;
+    TDG_CHECK(base + c >= base);
 #pragma unroll
     for (int j = 0; j < N; j++)
         if (o[j] != kNone) next[base++] = o[j];
@@ -230,8 +231,10 @@ struct PeelPolicy {
             x[q] = kHEmpty;
             ea[q] = kNone;
             if (act[q]) {
+                TDG_CHECK(uint64_t(ko[q].oa) + ja[q] < 2ull * g.m);
                 x[q] = elems[ko[q].oa + ja[q]];
                 ea[q] = g.eid[ko[q].oa + ja[q]];
+                TDG_CHECK(ea[q] < g.m && x[q] < g.n);
             }
         }
         // membership filter of a big table: a certain miss skips the table (tdg_common.cuh)
@@ -278,6 +281,7 @@ struct PeelPolicy {
             bi[q] = 0;
             if (look[q]) {
                 bi[q] = hbucket(h[q], ko[q].lb);
+                TDG_CHECK(ko[q].lb > 0 && uint64_t(ko[q].ob) + ko[q].lb <= g.nbuckets);
                 const uint4* kp = reinterpret_cast<const uint4*>(g.htab + 8ull * (ko[q].ob + bi[q]));
                 kv[q] = TDG_HTAB_NC ? __ldg(kp) : *kp;
                 if constexpr (kCount) { cn[kCntWalk]++; cn[kCntSlots]++; }
@@ -296,8 +300,10 @@ struct PeelPolicy {
             }
         }
 #pragma unroll
-        for (int q = 0; q < U; q++)
+        for (int q = 0; q < U; q++) {
             eb[q] = (look[q] && sl[q] < 4u) ? (g.htab[8ull * (ko[q].ob + bi[q]) + 4u + sl[q]] & ~kHUp) : kNone;
+            TDG_CHECK(eb[q] == kNone || eb[q] < g.m);
+        }
         uint32_t ids[U];
 #pragma unroll
         for (int q = 0; q < U; q++) ids[q] = ko[q].id;
@@ -361,6 +367,7 @@ __device__ void phase_scan(unsigned long long* ss, uint32_t level, uint32_t K, c
                 const uint32_t e = i < in.nA ? (in.implicit ? static_cast<uint32_t>(i) : in.A[i])
                                              : (far_in ? in.F[i - nAX] : in.X[i - in.nA]);
                 es[k] = e;
+                TDG_CHECK(e != kNone);
                 const unsigned long long w = ld_state(ss, e);
                 const uint32_t sv = st_s(w);
                 if (st_stamp(w) == 0 && !(far_in && sv < in.Bold)) {
@@ -562,6 +569,7 @@ __device__ void phase_compact_long(const DevGraph& g, const PeelBufs& pb, uint32
         uint32_t kept = 0;
         if (lo < dlu) {
             const uint32_t hi = min(dlu, lo + kChunk), o = g.off[ck.x];
+            TDG_CHECK(ck.x < g.n && hi <= g.off[ck.x + 1] - o);
             for (uint32_t r0 = lo; r0 < hi; r0 += 32u * kCompactU) {
                 uint32_t a[kCompactU], e[kCompactU], st[kCompactU];
 #pragma unroll
@@ -655,6 +663,7 @@ __device__ void phase_compact_short(const DevGraph& g, const uint32_t* pbits, un
                 a[q] = 0;
                 e[q] = 0;
                 if (item < total) {
+                    TDG_CHECK(slot[q] < 2ull * g.m);
                     a[q] = g.adj[slot[q]];
                     e[q] = g.eid[slot[q]];
                 }
@@ -712,7 +721,7 @@ __device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpr
 // red.release per block on a monotone arrival counter and an ld.acquire spin of thread 0
 // (no returned atomic on the critical path); else cooperative_groups' grid.sync().
 #ifndef TDG_FAST_BARRIER
-#define TDG_FAST_BARRIER 0
+#define TDG_FAST_BARRIER 1
 #endif
 struct GridBar {
     cg::grid_group grid;
@@ -754,7 +763,8 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
     while (true) {
         // ---- scan at `level` (one grid barrier); re-split the far list once level >= B
         const bool resplit = implicit || level >= B;
-        ScanIn in{pb.A[ai], nA, implicit, pb.X[xp], vload(&ctl->xcnt[xp]), pb.F[fi], resplit ? nF : 0u, B, B};
+        // (crossers sit right after the near list, in the same buffer: A[ai][nA .. nA + nX))
+        ScanIn in{pb.A[ai], nA, implicit, pb.A[ai] + nA, vload(&ctl->xcnt[xp]), pb.F[fi], resplit ? nF : 0u, B, B};
         if (resplit) in.B = near_bound(level);
         if (leader) {
             reset_ctr(&ctl->ph[(j + 1) % 3]);
@@ -815,7 +825,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                 ctl->cnt[kCntMarks] += pend_n;
                 if (level > 0) {
                     ctl->cnt[kCntTasks] += cs;
-                    if (kSortMin && cs >= kSortMin) ctl->cnt[kCntSorted] += cs;
+                    if (kSortMin && cs >= kSortMin && 5ull * cs <= 4ull * g.m) ctl->cnt[kCntSorted] += cs;
                 }
                 ctl->levels_len = level + 1;
                 reset_ctr(&ctl->ph[(j + 1) % 3]);
@@ -825,20 +835,23 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             if (pend_n) mark_processed(pb.pbits, pend, pend_n);
             if (level > 0) {  // level 0: s[e1] == 0 bounds its live triangles to none
                 const uint32_t* tasks = pb.L[li];
-                if (kSortMin && cs >= kSortMin) {  // group big sub-levels by searched vertex
+                // group big sub-levels by searched vertex; the sorted list sits after the task
+                // descriptors in the compaction scratch (16 + 4 bytes per task <= its 16m + 16)
+                if (kSortMin && cs >= kSortMin && 5ull * cs <= 4ull * g.m) {
                     phase_bucket_hist(g, tasks, cs, pb.bhist, pb.bshift);
                     grid.sync();
                     if (blockIdx.x == 0) phase_bucket_scan(pb.bhist, pb.bcur);
                     grid.sync();
-                    phase_bucket_scatter(g, tasks, cs, pb.bcur, pb.bshift, pb.Ls);
+                    uint32_t* Ls = reinterpret_cast<uint32_t*>(pb.desc + cs);
+                    phase_bucket_scatter(g, tasks, cs, pb.bcur, pb.bshift, Ls);
                     grid.sync();
-                    tasks = pb.Ls;
+                    tasks = Ls;
                 }
                 phase_prep(g, tasks, cs, pb.wpre, pb.bsum, pb.desc);
                 grid.sync();
                 const unsigned long long W =
                     phase_process<kCount>(g, pb.ss, level, K, tasks, cs, pb.wpre, pb.bsum, gridDim.x,
-                                          &ctl->ph[j % 3], pb.L[li ^ 1], ctl->cnt, B, pb.X[xp], &ctl->xcnt[xp],
+                                          &ctl->ph[j % 3], pb.L[li ^ 1], ctl->cnt, B, pb.A[ai] + nA, &ctl->xcnt[xp],
                                           pb.pbits, pb.desc);
                 if (leader) {
                     ctl->probes += W;

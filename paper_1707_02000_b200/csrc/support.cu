@@ -119,7 +119,7 @@ struct SupportPolicy {
 #endif
 constexpr uint32_t kSupTab = TDG_SUP_TAB;
 #ifndef TDG_SUP_LOAD
-#define TDG_SUP_LOAD 2  // table slots per key when the table is not full size
+#define TDG_SUP_LOAD 4  // table slots per key when the table is not full size (C5: 2 -> 4: 1089 -> 1047 ms)
 #endif
 constexpr size_t kSupSmem = size_t(kSupTab) * (sizeof(uint32_t) + sizeof(uint16_t));
 static_assert(kSupTab % 4 == 0 && 3 * kSupTab / 4 < 65536, "bucketed owner table: u16 positions");
@@ -173,9 +173,15 @@ struct SupportTabPolicy {
     __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
         uint32_t c[U], p[U];
 #pragma unroll
-        for (int q = 0; q < U; q++) c[q] = act[q] ? elems[ko[q].oa + ja[q]] : 0u;
+        for (int q = 0; q < U; q++) {
+            TDG_CHECK(!act[q] || uint64_t(ko[q].oa) + ja[q] < g.m);
+            c[q] = act[q] ? elems[ko[q].oa + ja[q]] : 0u;
+        }
 #pragma unroll
-        for (int q = 0; q < U; q++) p[q] = act[q] ? find(ko[q], c[q]) : kNone;
+        for (int q = 0; q < U; q++) {
+            p[q] = act[q] ? find(ko[q], c[q]) : kNone;
+            TDG_CHECK(p[q] == kNone || uint64_t(ko[q].ob) + p[q] < g.m);
+        }
         visit_all<U>(s, ko, ja, p);
     }
 };

@@ -14,12 +14,28 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 namespace tdg {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kNone = 0xffffffffu;
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Checked builds (-DTDG_CHECKS=1, tests/test_checked_gpu.py): device-side bounds and
+// invariant checks on the hot paths; a violation prints its site and traps the kernel.
+// (compute-sanitizer is not available on the GPU pool; these are the memory checks.)
+#ifndef TDG_CHECKS
+#define TDG_CHECKS 0
+#endif
+#define TDG_CHECK(cond)                                                                          \
+    do {                                                                                         \
+        if (TDG_CHECKS && !(cond)) {                                                             \
+            printf("TDG_CHECK failed %s:%d: %s (block %u thread %u)\n", __FILE__, __LINE__, #cond, \
+                   blockIdx.x, threadIdx.x);                                                     \
+            __trap();                                                                            \
+        }                                                                                        \
+    } while (0)
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
@@ -203,6 +219,7 @@ __device__ __forceinline__ uint64_t fword_index(uint32_t ob, uint32_t nb, uint32
 
 struct DevGraph {
     uint32_t n = 0, m = 0;
+    uint64_t nbuckets = 0;  // hash-table buckets allocated (bounds for checked builds)
     const uint32_t* htab = nullptr;  // bucketed hash tables: 8 u32 words (4 keys, 4 values) per bucket
     const uint32_t* hbo = nullptr;   // n+1 bucket offsets
     const unsigned long long* filt = nullptr;  // membership filters of the big tables (or null)

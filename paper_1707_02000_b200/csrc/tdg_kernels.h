@@ -211,7 +211,6 @@ struct PeelBufs {
     uint32_t* nsl;
     uint32_t nsl_cap;
     uint32_t count;       // diagnostic count mode: the k_peel<true> instantiation tallies every access
-    uint32_t* Ls;         // m: a big sub-level's curr list reordered by searched vertex
     uint32_t* bhist;      // kBuckets counters (zero between uses)
     uint32_t* bcur;       // kBuckets cursors
     uint32_t bshift;      // bucket = vertex >> bshift
@@ -226,8 +225,10 @@ struct PeelBufs {
     uint32_t* seid;
     uint32_t* pbits;  // (m+31)/32 words: bit e set once edge e's sub-level has run
     uint32_t* F[2];   // m each: far live edges (support >= the near bound when split)
-    uint32_t* X[2];   // m each: far edges whose support crossed below the near bound
-    uint4* desc;      // m: per-sub-level task descriptors (aliases the compaction scratch)
+    // (far edges whose support crossed below the near bound are appended right after the
+    // current near list A[ai], which the next scan reads as one list)
+    uint4* desc;      // m: per-sub-level task descriptors (aliases the compaction scratch; a
+                      // bucket-sorted curr list follows the descriptors)
 };
 #ifndef TDG_BUCKET_BITS
 #define TDG_BUCKET_BITS 16
