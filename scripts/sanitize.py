@@ -46,10 +46,10 @@ def main():
     cg = trussdec.CsrGraph.from_arrays(k4.offsets, k4.neighbors)
     tg = trussdec.build_truss_graph(cg)
     s = trussdec.support_am4(tg).copy()
-    f = trussdec.LevelFrontier(tg.m)
+    f = trussdec.LevelFrontier(tg.m())
     trussdec.scan(s, 2, f)
     bad += 0 if f.curr_size == 6 else 1
-    trussdec.process_sublevel(f, tg, s, 2, trussdec.MarkScratchPool(1, tg.n))
+    trussdec.process_sublevel(f, tg, s, 2, trussdec.MarkScratchPool(1, tg.n()))
     bad += 0 if (s == 2).all() and f.processed.sum() == 6 else 1
     # edge-list parser
     with tempfile.TemporaryDirectory() as d:
