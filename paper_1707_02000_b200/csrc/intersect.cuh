@@ -14,9 +14,18 @@
 // `visit(active, hit, task, ja, e)`; all 32 lanes call them together (warp collectives ok).
 #pragma once
 
+#include <type_traits>
+
 #include "tdg_common.cuh"
 
 namespace tdg {
+
+// Policy::flush() (optional): called by process_items after every piece, so a policy may
+// buffer work across engine steps (the peel's candidate queue).
+template <class P, class = void>
+struct has_flush : std::false_type {};
+template <class P>
+struct has_flush<P, std::void_t<decltype(std::declval<P&>().flush())>> : std::true_type {};
 
 // A task as the engine carries it between lanes (its item count lives in the work prefix).
 struct ITask {
@@ -297,6 +306,7 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
             guided_piece(p, W, nwarps, S0, minp, &x0, &x1);
             if (x0 >= W) break;
             run_items(P, x0, x1, task_at(x0, ntasks, wpre, sboff, nchunks, CH), ntasks, wpre, sboff, CH);
+            if constexpr (has_flush<Policy>::value) P.flush();
         }
         return W;
     }
@@ -313,6 +323,7 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
         const unsigned long long x0 = p * PS;
         const unsigned long long x1 = x0 + PS < W ? x0 + PS : W;
         run_items(P, x0, x1, task_at(x0, ntasks, wpre, sboff, nchunks, CH), ntasks, wpre, sboff, CH);
+        if constexpr (has_flush<Policy>::value) P.flush();
     }
     return W;
 }

@@ -132,6 +132,19 @@ __device__ __forceinline__ void emit_many(const uint32_t (&o)[N], uint32_t* ctr,
         if (o[j] != kNone) next[base++] = o[j];
 }
 
+// Two-stage probes (TDG_PEEL_QUEUE): stage A (list element + edge id, processed bit, filter
+// word — one level of independent random loads) pushes the ~1/3 of probes that survive into
+// a per-warp shared-memory queue; stage B drains it in full batches of kQBatch candidates
+// (table bucket -> value -> both peers' states -> atomics), so the long dependent chain runs
+// with every lane busy instead of once per step for the few lanes whose probe survived.
+#ifndef TDG_PEEL_QUEUE
+#define TDG_PEEL_QUEUE 1
+#endif
+constexpr int kQB = 3;                       // candidates per lane per drain
+constexpr uint32_t kQBatch = 32u * kQB;      // drain size
+constexpr uint32_t kQCap = 2u * kQBatch;     // < kQBatch left + <= 32 * TDG_PEEL_U new (<= kQBatch)
+static_assert(32 * TDG_PEEL_U <= int(kQBatch), "one engine step must fit behind a partial batch");
+
 // process_sublevel's inner loop (truss_parallel.cpp:80-88) as a probe-engine policy: a hit
 // is w in N(u) ∩ N(v): slot ja of the probe list (its eid is one peer) found in the other
 // endpoint's hash table (whose value is the other peer's id). kCount = the diagnostic
@@ -152,6 +165,8 @@ struct PeelPolicy {
     uint32_t* xcnt;
     const uint32_t* pbits;        // edges processed in earlier sub-levels (or null)
     const uint4* desc;            // task descriptors written by phase_prep
+    uint32_t* qbuf;               // this warp's candidate queue (TDG_PEEL_QUEUE): 5 x kQCap u32, SoA
+    uint32_t nq = 0;              // queued candidates (warp-uniform)
     static constexpr bool kFast = TDG_PEEL_FAST;
     static constexpr int kUnroll = TDG_PEEL_U;
     static_assert(kUnroll > 1, "the peel's probe loop is the U-chain form (run)");
@@ -223,7 +238,154 @@ struct PeelPolicy {
     // list element + its edge id (coalesced) -> first table slot -> (collisions) ->
     // both peers' state words -> both decrements -> one warp append for all targets.
     template <int U>
-    __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
+    __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) {
+        if constexpr (TDG_PEEL_QUEUE) run_queued<U>(act, ko, ja);
+        else run_fused<U>(act, ko, ja);
+    }
+    // Table lookup of key x in the table [ob, ob + lb) (hash h = hmix(x)): the partner edge id
+    // or kNone. One 16-byte key vector per bucket; the value (same sector) only on a hit.
+    __device__ __forceinline__ uint32_t table_find(uint32_t x, uint32_t h, uint32_t ob, uint32_t lb,
+                                                   uint32_t (&cn)[kCntProbe]) const {
+        uint32_t bi = hbucket(h, lb);
+        TDG_CHECK(lb > 0 && uint64_t(ob) + lb <= g.nbuckets);
+        uint4 kv = TDG_HTAB_NC ? __ldg(reinterpret_cast<const uint4*>(g.htab + 8ull * (ob + bi)))
+                               : *reinterpret_cast<const uint4*>(g.htab + 8ull * (ob + bi));
+        if constexpr (kCount) { cn[kCntWalk]++; cn[kCntSlots]++; }
+        uint32_t sl = bucket_find(kv, x);
+        while (sl == 4u && kv.w != kHEmpty) {  // home bucket full: the key may sit further on
+            bi = hnext(bi, lb);
+            kv = TDG_HTAB_NC ? __ldg(reinterpret_cast<const uint4*>(g.htab + 8ull * (ob + bi)))
+                             : *reinterpret_cast<const uint4*>(g.htab + 8ull * (ob + bi));
+            sl = bucket_find(kv, x);
+            if constexpr (kCount) cn[kCntSlots]++;
+        }
+        const uint32_t eb = sl < 4u ? (g.htab[8ull * (ob + bi) + 4u + sl] & ~kHUp) : kNone;
+        TDG_CHECK(eb == kNone || eb < g.m);
+        return eb;
+    }
+    __device__ __forceinline__ void flush_counts(uint32_t (&cn)[kCntProbe]) const {
+        if constexpr (kCount) {
+#pragma unroll
+            for (int k = 0; k < kCntProbe; k++) {
+                const uint32_t t = __reduce_add_sync(kFull, cn[k]);
+                if (lane_id() == 0 && t) atomicAdd(cnt + k, static_cast<unsigned long long>(t));
+            }
+        }
+    }
+    // Stage B: the first k (<= kQBatch) queued candidates -> table -> visit; the rest moves up.
+    __device__ void drain(uint32_t k) {
+        uint32_t* qx = qbuf;
+        uint32_t* qea = qbuf + kQCap;
+        uint32_t* qid = qbuf + 2 * kQCap;
+        uint32_t* qob = qbuf + 3 * kQCap;
+        uint32_t* qlb = qbuf + 4 * kQCap;
+        const uint32_t lane = lane_id();
+        uint32_t cn[kCntProbe] = {};
+        __syncwarp();
+        uint32_t x[kQB], ea[kQB], eb[kQB], ids[kQB], ob[kQB], lb[kQB];
+#pragma unroll
+        for (int r = 0; r < kQB; r++) {
+            const uint32_t i = lane + 32u * r;
+            eb[r] = kNone;
+            ea[r] = kNone;
+            ids[r] = kNone;
+            if (i < k) {
+                x[r] = qx[i];
+                ea[r] = qea[i];
+                ids[r] = qid[i];
+                ob[r] = qob[i];
+                lb[r] = qlb[i];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kQB; r++)
+            if (lane + 32u * r < k) eb[r] = table_find(x[r], hmix(x[r]), ob[r], lb[r], cn);
+        apply<kQB>(ea, eb, ids, cn);
+        flush_counts(cn);
+        // move the leftover [k, nq) (< kQBatch entries, disjoint from [0, k)) to the front
+        const uint32_t left = nq - k;
+        __syncwarp();
+        for (uint32_t i = lane; i < left; i += 32) {
+            qx[i] = qx[k + i];
+            qea[i] = qea[k + i];
+            qid[i] = qid[k + i];
+            qob[i] = qob[k + i];
+            qlb[i] = qlb[k + i];
+        }
+        __syncwarp();
+        nq = left;
+    }
+    __device__ void flush() {
+        if constexpr (TDG_PEEL_QUEUE)
+            if (nq) drain(nq);
+    }
+    // Stage A of U probes per lane: survivors of the processed bit and the filter are queued.
+    template <int U>
+    __device__ void run_queued(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) {
+        uint32_t x[U], ea[U], h[U];
+        uint32_t cn[kCntProbe] = {};
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            x[q] = kHEmpty;
+            ea[q] = kNone;
+            if (act[q]) {
+                TDG_CHECK(uint64_t(ko[q].oa) + ja[q] < 2ull * g.m);
+                x[q] = elems[ko[q].oa + ja[q]];
+                ea[q] = g.eid[ko[q].oa + ja[q]];
+                TDG_CHECK(ea[q] < g.m && x[q] < g.n);
+            }
+        }
+        bool look[U];
+        uint32_t pw[U];
+        unsigned long long fw[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            look[q] = act[q];
+            h[q] = look[q] ? hmix(x[q]) : 0u;
+            pw[q] = (pbits && look[q]) ? pbits[ea[q] >> 5] : 0u;
+            if constexpr (kCount) cn[kCntPbits] += (pbits && look[q]) ? 1u : 0u;
+            fw[q] = ~0ull;
+            if (g.filt && look[q] && ko[q].lb >= kFMin) {
+                fw[q] = __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q]));
+                if constexpr (kCount) cn[kCntFilter]++;
+            }
+        }
+        uint32_t* qx = qbuf;
+        uint32_t* qea = qbuf + kQCap;
+        uint32_t* qid = qbuf + 2 * kQCap;
+        uint32_t* qob = qbuf + 3 * kQCap;
+        uint32_t* qlb = qbuf + 4 * kQCap;
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const unsigned long long fb = fbits(h[q]);
+            if ((fw[q] & fb) != fb) look[q] = false;
+            if ((pw[q] >> (ea[q] & 31u)) & 1u) look[q] = false;
+            const uint32_t bal = __ballot_sync(kFull, look[q]);
+            if (look[q]) {
+                const uint32_t pos = nq + __popc(bal & lanemask_lt());
+                qx[pos] = x[q];
+                qea[pos] = ea[q];
+                qid[pos] = ko[q].id;
+                qob[pos] = ko[q].ob;
+                qlb[pos] = ko[q].lb;
+            }
+            nq += __popc(bal);
+        }
+        if constexpr (kCount) {
+#pragma unroll
+            for (int q = 0; q < U; q++) {
+                if (act[q]) {
+                    const uint32_t sa = st_stamp(ld_state(ss, ea[q]));
+                    cn[kCntDead] += (sa != 0 && sa < K) ? 1u : 0u;
+                }
+            }
+        }
+        flush_counts(cn);
+        if (nq >= kQBatch) drain(kQBatch);
+    }
+    // Fused form (TDG_PEEL_QUEUE = 0): each lane's U probes run the whole chain in one step.
+    template <int U>
+    __device__ void run_fused(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
         uint32_t x[U], ea[U], eb[U], h[U];
         uint32_t cn[kCntProbe] = {};  // per-lane access tallies (kCount only; folded away otherwise)
 #pragma unroll
@@ -531,7 +693,9 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             unsigned long long* cnt, uint32_t B, uint32_t* X, uint32_t* xcnt,
                                             const uint32_t* pbits, const uint4* desc) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
-    PeelPolicy<kCount> P{g, ss, level, K, curr, ph, next, g.adj, cnt, B, X, xcnt, pbits, desc};
+    __shared__ uint32_t squeue[TDG_PEEL_QUEUE ? kWarps * 5 * kQCap : 1];
+    PeelPolicy<kCount> P{g, ss, level, K, curr, ph, next, g.adj, cnt, B, X, xcnt, pbits, desc,
+                         squeue + (TDG_PEEL_QUEUE ? (threadIdx.x >> 5) * 5 * kQCap : 0)};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
 }
 
