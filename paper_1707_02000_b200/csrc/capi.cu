@@ -86,7 +86,6 @@ bool peel_filter();
 struct tdg_context {
     int device = 0;
     int sms = 148;
-    size_t l2_persist = 0;  // persisting L2 set-aside reserved on the device (bytes)
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     // persistent per-graph arrays (live through the peel)
@@ -253,7 +252,6 @@ struct tdg_context {
         p.seid = cscr + word / 2;  // 2 words later (word is in bytes: 2 * word / 4 u32)
         p.desc = reinterpret_cast<uint4*>(cscr);
         p.pbits = pbits.as<uint32_t>();
-        p.l2_persist_bytes = l2_persist;
         return p;
     }
     void trim() {
@@ -348,15 +346,6 @@ void create_ctx(int device, tdg_context** out) {
     c->device = device;
     c->sms = prop.multiProcessorCount;
     ck(cudaSetDevice(device), "cudaSetDevice");
-    // reserve the device's persisting L2 set-aside (the peel's processed bitmap uses it per
-    // launch; other accesses may use the set-aside while it is not claimed)
-    if (prop.persistingL2CacheMaxSize > 0) {
-        size_t cur = 0;
-        if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) == cudaSuccess && cur < size_t(prop.persistingL2CacheMaxSize))
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prop.persistingL2CacheMaxSize);
-        cudaDeviceGetLimit(&c->l2_persist, cudaLimitPersistingL2CacheSize);
-        cudaGetLastError();
-    }
     ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own;
     for (auto& ev : c->ev) ck(cudaEventCreate(&ev), "cudaEventCreate");

@@ -884,9 +884,6 @@ __device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpr
 // Grid-wide barrier of the persistent kernel. TDG_FAST_BARRIER: one fire-and-forget
 // red.release per block on a monotone arrival counter and an ld.acquire spin of thread 0
 // (no returned atomic on the critical path); else cooperative_groups' grid.sync().
-#ifndef TDG_L2_PERSIST
-#define TDG_L2_PERSIST 1  // processed bitmap as an L2 persisting window during the peel
-#endif
 #ifndef TDG_FAST_BARRIER
 #define TDG_FAST_BARRIER 1
 #endif
@@ -1154,30 +1151,19 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     DevGraph gg = g;
     PeelBufs pp = p;
     void* args[] = {&gg, &pp};
-    // one cooperative launch; with TDG_L2_PERSIST the processed-edge bitmap (m bits, read by
-    // every probe) is an L2 persisting window for this launch only (the device's persisting
-    // set-aside is reserved once per context, capi.cu)
+    // one cooperative launch (an L2 persisting window on the processed bitmap was measured
+    // here: the device-wide set-aside it needs shrank the normal L2 for every kernel, C5 peel
+    // 2.52 -> 3.77 s and build 145 -> 252 ms; removed)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(kPeelThreads);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[1];
     unsigned na = 0;
     at[na].id = cudaLaunchAttributeCooperative;
     at[na].val.cooperative = 1;
     na++;
-    if (TDG_L2_PERSIST && p.pbits && p.l2_persist_bytes) {
-        const size_t bytes = size_t((g.m + 31) / 32) * 4;
-        at[na].id = cudaLaunchAttributeAccessPolicyWindow;
-        at[na].val.accessPolicyWindow.base_ptr = p.pbits;
-        at[na].val.accessPolicyWindow.num_bytes = bytes;
-        at[na].val.accessPolicyWindow.hitRatio =
-            bytes <= p.l2_persist_bytes ? 1.0f : static_cast<float>(double(p.l2_persist_bytes) / double(bytes));
-        at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        na++;
-    }
     cfg.attrs = at;
     cfg.numAttrs = na;
     err = cudaLaunchKernelExC(&cfg, kern, args);

@@ -224,7 +224,6 @@ struct PeelBufs {
     uint32_t* sadj;
     uint32_t* seid;
     uint32_t* pbits;  // (m+31)/32 words: bit e set once edge e's sub-level has run
-    size_t l2_persist_bytes;  // device L2 persisting set-aside (0: no persisting window)
     uint32_t* F[2];   // m each: far live edges (support >= the near bound when split)
     // (far edges whose support crossed below the near bound are appended right after the
     // current near list A[ai], which the next scan reads as one list)
