@@ -221,7 +221,8 @@ enum {
     TDG_CNT_MARKS,          /* peel: processed-bitmap marks                                */
     TDG_CNT_SUP_TAB_ELEMS,  /* support: N+(owner) elements loaded into shared-memory tables */
     TDG_CNT_SUP_SEGMENTS,   /* support: owner segments served from a shared-memory table   */
-    TDG_CNT_SUP_SEARCH,     /* support: probe items binary-searched in global memory       */
+    TDG_CNT_SUP_SEARCH,     /* support: 16-byte list quads binary-searched in global memory */
+    TDG_CNT_SUP_HUB,        /* support: quads x passes of owners whose N+ exceeds one table */
     TDG_NCOUNTERS
 };
 int tdg_counters(tdg_context* ctx, uint64_t* out, uint64_t cap);

@@ -1027,6 +1027,7 @@ int tdg_counters(tdg_context* ctx, uint64_t* out, uint64_t cap) {
         v[TDG_CNT_SUP_TAB_ELEMS] = c->hctl->sup.tab_elems;
         v[TDG_CNT_SUP_SEGMENTS] = c->hctl->sup.tab_segments;
         v[TDG_CNT_SUP_SEARCH] = c->hctl->sup.search_items;
+        v[TDG_CNT_SUP_HUB] = c->hctl->sup.hub_items;
         for (uint64_t i = 0; i < cap && i < TDG_NCOUNTERS; i++) out[i] = v[i];
     });
 }

@@ -27,6 +27,12 @@ struct has_flush : std::false_type {};
 template <class P>
 struct has_flush<P, std::void_t<decltype(std::declval<P&>().flush())>> : std::true_type {};
 
+// Policy::kRunForm (optional, true): the policy takes whole steps through run<U> even at U = 1.
+template <class P, class = void>
+struct has_run_form : std::false_type {};
+template <class P>
+struct has_run_form<P, std::enable_if_t<P::kRunForm>> : std::true_type {};
+
 // A task as the engine carries it between lanes (its item count lives in the work prefix).
 struct ITask {
     uint32_t id;      // peel: e1 ; support: edge id of the oriented edge a->b
@@ -180,7 +186,7 @@ __device__ __forceinline__ void run_items(Policy& P, unsigned long long x0, unsi
         // peel's U = 3 probe loop is register-bound and loses more to the cache than it saves.)
         const uint32_t r1 = Policy::kFast ? __shfl_sync(kFull, relk, 1) : 0u;
         const bool one = Policy::kFast && r1 >= 32u * U;
-        if constexpr (U > 1) {
+        if constexpr (U > 1 || has_run_form<Policy>::value) {
             // U items per lane per step (item base + lane + 32q): the policy issues their
             // independent loads together, so each lane keeps U probe chains in flight.
             ITask ko[U];
@@ -298,15 +304,22 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
         unsigned long long S0 = (W + 2ull * nwarps - 1) / (2ull * nwarps);
         S0 = (S0 + kStep - 1) / kStep * kStep;
         const unsigned long long minp = kStep > TDG_MIN_PIECE ? kStep : TDG_MIN_PIECE;
+        // The first piece of every warp is static (piece = warp index, warp 0 of every block
+        // first so a small phase spreads over the SMs); only the pieces after that first tier
+        // are pulled from the counter. A small phase therefore issues no atomics at all (one
+        // same-address atomic per warp was ~5 us of every small sub-level).
+        unsigned long long x0, x1;
+        guided_piece(nwarps, W, nwarps, S0, minp, &x0, &x1);
+        const bool dynamic = x0 < W;
+        uint32_t p = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
         while (true) {
-            uint32_t p = 0;
-            if (lane == 0) p = atomicAdd(piece_head, 1u);
-            p = __shfl_sync(kFull, p, 0);
-            unsigned long long x0, x1;
             guided_piece(p, W, nwarps, S0, minp, &x0, &x1);
             if (x0 >= W) break;
             run_items(P, x0, x1, task_at(x0, ntasks, wpre, sboff, nchunks, CH), ntasks, wpre, sboff, CH);
             if constexpr (has_flush<Policy>::value) P.flush();
+            if (!dynamic) break;
+            if (lane == 0) p = nwarps + atomicAdd(piece_head, 1u);
+            p = __shfl_sync(kFull, p, 0);
         }
         return W;
     }

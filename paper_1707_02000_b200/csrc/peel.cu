@@ -68,6 +68,12 @@ constexpr int kWarps = kPeelThreads / 32;
 #ifndef TDG_PEEL_FAST
 #define TDG_PEEL_FAST 0  // engine fast path (intersect.cuh) for the peel's probe loop
 #endif
+#ifndef TDG_DIAG_RATIO
+#define TDG_DIAG_RATIO 0  // diagnostic build: probe-weighted task-shape histograms, printed by the kernel
+#endif
+#if TDG_DIAG_RATIO
+__device__ unsigned long long d_diag[16];
+#endif
 // la = the probe count (live length of the shorter list).
 __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1, uint32_t& la) {
     const uint2 p = g.el[e1];
@@ -78,6 +84,16 @@ __device__ __forceinline__ ITask ptask(const DevGraph& g, uint32_t e1, uint32_t&
     k.id = e1;
     k.oa = g.off[a];
     la = pu ? du : dv;
+#if TDG_DIAG_RATIO
+    {   // probe-weighted histograms of (searched live length / probe length) and of the searched length
+        const uint32_t lbv = pu ? dv : du, r = la ? lbv / la : 0;
+        const int rc = r < 2 ? 0 : r < 4 ? 1 : r < 8 ? 2 : r < 16 ? 3 : r < 64 ? 4 : 5;
+        const int sc = lbv < 512 ? 0 : lbv < 2048 ? 1 : lbv < 8192 ? 2 : lbv < 32768 ? 3 : lbv < 131072 ? 4 : lbv < 524288 ? 5 : 6;
+        atomicAdd(&d_diag[rc], static_cast<unsigned long long>(la));
+        atomicAdd(&d_diag[6 + sc], static_cast<unsigned long long>(la));
+        if (r < 8) atomicAdd(&d_diag[13 + (sc < 3 ? 0 : sc < 5 ? 1 : 2)], static_cast<unsigned long long>(la));
+    }
+#endif
     k.ob = g.hbo[b];
     k.lb = g.hbo[b + 1] - k.ob;
     return k;
@@ -684,6 +700,18 @@ __device__ __forceinline__ bool processed_bit(const uint32_t* pbits, uint32_t e)
     return (ld_relaxed(pbits + (e >> 5)) >> (e & 31)) & 1u;
 }
 
+// Shared memory of the sub-level phases (one instance per block): the chunk offsets of the
+// work prefix (or, in a fused small sub-level, its whole prefix and task descriptors) and the
+// warps' candidate queues.
+struct PeelShared {
+    unsigned long long sboff[kMaxChunks + 1];
+    uint32_t squeue[TDG_PEEL_QUEUE ? kWarps * 5 * kQCap : 1];
+};
+__device__ __forceinline__ PeelShared& peel_shared() {
+    __shared__ __align__(16) PeelShared sh;
+    return sh;
+}
+
 // process_sublevel (truss_parallel.cpp:39-104) for curr[0..cs) on the intersection engine.
 template <bool kCount>
 __device__ unsigned long long phase_process(const DevGraph& g, unsigned long long* ss, uint32_t level,
@@ -692,11 +720,43 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
                                             uint32_t nchunks, PhaseCtr* ph, uint32_t* next,
                                             unsigned long long* cnt, uint32_t B, uint32_t* X, uint32_t* xcnt,
                                             const uint32_t* pbits, const uint4* desc) {
-    __shared__ unsigned long long sboff[kMaxChunks + 1];
-    __shared__ uint32_t squeue[TDG_PEEL_QUEUE ? kWarps * 5 * kQCap : 1];
+    PeelShared& sh = peel_shared();
     PeelPolicy<kCount> P{g, ss, level, K, curr, ph, next, g.adj, cnt, B, X, xcnt, pbits, desc,
-                         squeue + (TDG_PEEL_QUEUE ? (threadIdx.x >> 5) * 5 * kQCap : 0)};
-    return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sboff);
+                         sh.squeue + (TDG_PEEL_QUEUE ? (threadIdx.x >> 5) * 5 * kQCap : 0)};
+    return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sh.sboff);
+}
+
+// Small sub-levels (cs <= kFuseMax tasks: most of the thousands of late sub-levels) run prep
+// and process as ONE phase: every block resolves all task descriptors itself (one task per
+// thread) into shared memory and scans their probe counts there, then runs the usual
+// process phase on that one-chunk prefix — no work-prefix round trip through global memory,
+// one grid barrier per sub-level instead of two (and no piece-counter atomics: the first
+// tier of pieces is static). Same probes, same sets.
+#ifndef TDG_FUSE_MAX
+#define TDG_FUSE_MAX 256
+#endif
+constexpr uint32_t kFuseMax = TDG_FUSE_MAX;
+static_assert(kFuseMax <= uint32_t(kPeelThreads), "fused prep: one task per thread");
+// layout inside PeelShared::sboff (u64 words): [0,1] chunk offsets of the one chunk, [2] its
+// total (the "bsum"), [8, 8 + kFuseMax) the prefix, then the descriptors (16-byte aligned)
+constexpr uint32_t kFusePre = 8, kFuseDesc = 8 + kFuseMax + (kFuseMax & 1);
+static_assert((kFuseDesc * 8) % 16 == 0 && kFuseDesc * 8 + kFuseMax * 16 <= (kMaxChunks + 1) * 8,
+              "fused prefix + descriptors alias the chunk-offset array");
+
+__device__ void phase_fused_prep(const DevGraph& g, const uint32_t* curr, uint32_t cs) {
+    PeelShared& sh = peel_shared();
+    uint4* sdesc = reinterpret_cast<uint4*>(sh.sboff + kFuseDesc);
+    const uint32_t t = threadIdx.x;
+    uint32_t la = 0;
+    if (t < cs) {
+        const ITask k = ptask(g, curr[t], la);
+        sdesc[t] = make_uint4(k.id, k.oa, k.ob, k.lb);
+    }
+    unsigned long long W;
+    const unsigned long long ex = block_excl_scan64<kPeelThreads>(la, W);
+    if (t < cs) sh.sboff[kFusePre + t] = ex;
+    if (t == 0) sh.sboff[2] = W;
+    __syncthreads();
 }
 
 // Adjacency compaction (between levels): drop processed edges (0 < stamp < K) from every
@@ -999,24 +1059,36 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             if (pend_n) mark_processed(pb.pbits, pend, pend_n);
             if (level > 0) {  // level 0: s[e1] == 0 bounds its live triangles to none
                 const uint32_t* tasks = pb.L[li];
-                // group big sub-levels by searched vertex; the sorted list sits after the task
-                // descriptors in the compaction scratch (16 + 4 bytes per task <= its 16m + 16)
-                if (kSortMin && cs >= kSortMin && 5ull * cs <= 4ull * g.m) {
-                    phase_bucket_hist(g, tasks, cs, pb.bhist, pb.bshift);
+                const unsigned long long* wp = pb.wpre;
+                const unsigned long long* bs = pb.bsum;
+                const uint4* dsc = pb.desc;
+                uint32_t nch = gridDim.x;
+                if (kFuseMax && cs <= kFuseMax) {
+                    phase_fused_prep(g, tasks, cs);
+                    PeelShared& sh = peel_shared();
+                    wp = sh.sboff + kFusePre;
+                    bs = sh.sboff + 2;
+                    dsc = reinterpret_cast<const uint4*>(sh.sboff + kFuseDesc);
+                    nch = 1;
+                } else {
+                    // group big sub-levels by searched vertex; the sorted list sits after the task
+                    // descriptors in the compaction scratch (16 + 4 bytes per task <= its 16m + 16)
+                    if (kSortMin && cs >= kSortMin && 5ull * cs <= 4ull * g.m) {
+                        phase_bucket_hist(g, tasks, cs, pb.bhist, pb.bshift);
+                        grid.sync();
+                        if (blockIdx.x == 0) phase_bucket_scan(pb.bhist, pb.bcur);
+                        grid.sync();
+                        uint32_t* Ls = reinterpret_cast<uint32_t*>(pb.desc + cs);
+                        phase_bucket_scatter(g, tasks, cs, pb.bcur, pb.bshift, Ls);
+                        grid.sync();
+                        tasks = Ls;
+                    }
+                    phase_prep(g, tasks, cs, pb.wpre, pb.bsum, pb.desc);
                     grid.sync();
-                    if (blockIdx.x == 0) phase_bucket_scan(pb.bhist, pb.bcur);
-                    grid.sync();
-                    uint32_t* Ls = reinterpret_cast<uint32_t*>(pb.desc + cs);
-                    phase_bucket_scatter(g, tasks, cs, pb.bcur, pb.bshift, Ls);
-                    grid.sync();
-                    tasks = Ls;
                 }
-                phase_prep(g, tasks, cs, pb.wpre, pb.bsum, pb.desc);
-                grid.sync();
                 const unsigned long long W =
-                    phase_process<kCount>(g, pb.ss, level, K, tasks, cs, pb.wpre, pb.bsum, gridDim.x,
-                                          &ctl->ph[j % 3], pb.L[li ^ 1], ctl->cnt, B, pb.A[ai] + nA, &ctl->xcnt[xp],
-                                          pb.pbits, pb.desc);
+                    phase_process<kCount>(g, pb.ss, level, K, tasks, cs, wp, bs, nch, &ctl->ph[j % 3], pb.L[li ^ 1],
+                                          ctl->cnt, B, pb.A[ai] + nA, &ctl->xcnt[xp], pb.pbits, dsc);
                 if (leader) {
                     ctl->probes += W;
                     sub_w = W;
@@ -1048,6 +1120,16 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         level++;
     }
     if (leader) ctl->final_stamp = K;
+#if TDG_DIAG_RATIO
+    if (leader) {
+        printf("DIAG ratio lb/la (<2,<4,<8,<16,<64,>=64):");
+        for (int i = 0; i < 6; i++) printf(" %llu", d_diag[i]);
+        printf("\nDIAG lb (<512,<2K,<8K,<32K,<128K,<512K,>=512K):");
+        for (int i = 6; i < 13; i++) printf(" %llu", d_diag[i]);
+        printf("\nDIAG ratio<8 by lb (<8K,<128K,>=128K): %llu %llu %llu\n", d_diag[13], d_diag[14], d_diag[15]);
+        for (int i = 0; i < 16; i++) d_diag[i] = 0;
+    }
+#endif
 }
 
 __global__ void k_peel_init(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ dl,

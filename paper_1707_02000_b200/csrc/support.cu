@@ -25,104 +25,114 @@ namespace {
 constexpr int kThreads = 256;
 
 // Task t = slot j of owner x (build.cu k_svalid): the oriented edge {x, y} whose longer N+
-// list is x's. Probe N+(y) (coalesced, min(d+) items) and binary-search each element in
-// N+(x); tasks are grouped by x, so consecutive tasks search the same L1-resident list.
+// list is x's. N+(y) (min(d+) elements) is read as 16-byte QUADS — the work items of the
+// engine are the aligned 4-element groups that cover the list, one LDG.E.128 per item — and
+// every element is looked up in N+(x); tasks are grouped by x. Oriented lists are at most
+// sqrt(2m) < 2^16 long, so both lengths share one word: lb = d+(y) << 16 | d+(x).
 __device__ __forceinline__ ITask otask(const DevGraph& g, uint32_t t) {
     const uint32_t j = g.stask[t], x = g.sx[t], y = g.adj[j];
     ITask k;
     k.id = g.eid[j];
     k.oa = g.opos[y];
     k.ob = g.opos[x];
-    k.lb = g.opos[x + 1] - k.ob;
+    const uint32_t ly = g.opos[y + 1] - k.oa, lx = g.opos[x + 1] - k.ob;
+    TDG_CHECK(ly < 65536u && lx < 65536u);
+    k.lb = (ly << 16) | lx;
     return k;
+}
+// Quads covering the list [oa, oa + len) of a 16-byte-aligned array.
+__device__ __forceinline__ uint32_t quads_of(uint32_t oa, uint32_t len) {
+    return len ? ((oa & 3u) + len + 3u) >> 2 : 0u;
 }
 
 // Edge ids are internal (build.cu launch_internal_ids): an edge's id IS its oriented slot
-// (position in the N+ arrays). The owner-side slots of a task group are one contiguous,
-// L2-resident N+(x) range and the probe-side slots of one task are consecutive, so the
-// per-triangle atomics stay out of DRAM (reference-id-indexed atomics were random 2 GB
-// read-modify-writes at C5).
-// Hits of one engine step (U items per lane): each hit closes triangle {x, y, c} — the
-// oriented slots of y->c and x->c get one atomic each; the tasks' own edges are counted
-// with one atomic per step when every lane works on the same task (the common case in
-// long lists), else per item with one atomic per group of lanes sharing a task.
-template <int U>
-__device__ __forceinline__ void visit_all(uint32_t* s, const ITask (&ko)[U], const uint32_t (&ja)[U],
-                                          const uint32_t (&p)[U]) {
-    uint32_t tot = 0;
-    bool same = true;
-    const uint32_t id0 = __shfl_sync(kFull, ko[0].id, 0);
-#pragma unroll
-    for (int q = 0; q < U; q++) {
-        const bool hit = p[q] != kNone;
-        if (hit) {
-            atomicAdd(&s[ko[q].oa + ja[q]], 1u);
-            atomicAdd(&s[ko[q].ob + p[q]], 1u);
-        }
-        tot += __popc(__ballot_sync(kFull, hit));
-        same = same && (!hit || ko[q].id == id0);
-    }
-    if (tot == 0) return;
-    if (__all_sync(kFull, same)) {
-        if (lane_id() == 0) atomicAdd(&s[id0], tot);
+// (position in the N+ arrays). The owner-side slots of a task group are one contiguous
+// N+(x) range and the probe-side slots of one task are consecutive, so the per-triangle
+// atomics stay out of DRAM (reference-id-indexed atomics were random 2 GB read-modify-writes
+// at C5).
+// Own-edge counts of one engine step: hq = this lane's hits in its quad of task `id`; one
+// atomic per step when every hit belongs to one task (the common case in long lists), else
+// one per group of lanes sharing a task (hq <= 4: three bit-plane ballots give a group's sum).
+__device__ __forceinline__ void count_own(uint32_t* s, uint32_t id, uint32_t hq) {
+    const uint32_t hm = __ballot_sync(kFull, hq != 0);
+    if (!hm) return;
+    const uint32_t leader = __ffs(hm) - 1;
+    const uint32_t id0 = __shfl_sync(kFull, id, leader);
+    if (__all_sync(kFull, hq == 0 || id == id0)) {
+        const uint32_t tot = __reduce_add_sync(kFull, hq);
+        if (lane_id() == leader) atomicAdd(&s[id0], tot);
         return;
     }
-#pragma unroll
-    for (int q = 0; q < U; q++) {
-        const bool hit = p[q] != kNone;
-        const uint32_t fm = __ballot_sync(kFull, hit);
-        if (fm && hit) {
-            const uint32_t grp = __match_any_sync(fm, ko[q].id);
-            if (lane_id() == static_cast<uint32_t>(__ffs(grp) - 1))
-                atomicAdd(&s[ko[q].id], static_cast<uint32_t>(__popc(grp)));
-        }
+    if (hq) {
+        const uint32_t grp = __match_any_sync(hm, id);
+        const uint32_t b0 = __ballot_sync(hm, hq & 1u), b1 = __ballot_sync(hm, hq & 2u), b2 = __ballot_sync(hm, hq & 4u);
+        const uint32_t sum = __popc(b0 & grp) + 2u * __popc(b1 & grp) + 4u * __popc(b2 & grp);
+        if (lane_id() == static_cast<uint32_t>(__ffs(grp) - 1)) atomicAdd(&s[id], sum);
     }
 }
 
 #ifndef TDG_SUP_U
-#define TDG_SUP_U 2  // probe items per lane per engine step in the support pass
+#define TDG_SUP_U 2  // quads per lane per engine step in the support pass (8 probes per lane)
 #endif
+// Search form (segments too small to pay for a table): every element of the quad is
+// binary-searched in N+(x) in global memory.
 struct SupportPolicy {
     const DevGraph& g;
     uint32_t* s;
     const uint32_t* elems;
     static constexpr bool kFast = true;
+    static constexpr bool kRunForm = true;
     static constexpr int kUnroll = TDG_SUP_U;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
-    __device__ uint32_t find(const ITask& k, uint32_t x) const {
-        const uint32_t p = lower_bound_u32(g.oadj + k.ob, k.lb, x);
-        return (p < k.lb && g.oadj[k.ob + p] == x) ? p : kNone;
-    }
-    // U items per lane per engine step: the U list loads and lookups issue together and
-    // the engine's per-step bookkeeping is amortised over 32U probes.
     template <int U>
     __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
-        uint32_t c[U], p[U];
+        uint4 v[U];
+        uint32_t base[U];
 #pragma unroll
-        for (int q = 0; q < U; q++) c[q] = act[q] ? elems[ko[q].oa + ja[q]] : 0u;
+        for (int q = 0; q < U; q++) {
+            base[q] = (ko[q].oa & ~3u) + 4u * ja[q];
+            v[q] = act[q] ? __ldg(reinterpret_cast<const uint4*>(elems + base[q])) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-        for (int q = 0; q < U; q++) p[q] = act[q] ? find(ko[q], c[q]) : kNone;
-        visit_all<U>(s, ko, ja, p);
+        for (int q = 0; q < U; q++) {
+            const uint32_t c[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+            const uint32_t ly = ko[q].lb >> 16, lx = ko[q].lb & 0xffffu;
+            uint32_t hq = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const uint32_t idx = base[q] + e;
+                if (act[q] && idx - ko[q].oa < ly) {  // (unsigned: also drops idx < oa)
+                    const uint32_t p = lower_bound_u32(g.oadj + ko[q].ob, lx, c[e]);
+                    if (p < lx && g.oadj[ko[q].ob + p] == c[e]) {
+                        atomicAdd(&s[idx], 1u);
+                        atomicAdd(&s[ko[q].ob + p], 1u);
+                        hq++;
+                    }
+                }
+            }
+            count_own(s, ko[q].id, hq);
+        }
     }
 };
 
 // ---- owner-table form. A block takes a piece of the work axis and walks its owner
 // segments (the tasks of one owner x are contiguous, [sbeg[x], sbeg[x+1])). For a segment
-// with enough work, N+(x) is loaded once into a shared-memory hash table (key c -> its
-// position in N+(x)) and the block's 8 warps split the segment's items evenly; each probe is then
-// one coalesced N+(y) load plus ~1 shared-memory access instead of a log2(d+(x)) chain of
-// L1 loads (the search form is issue-bound: ncu C3, 71% issue slots busy). Segments that
-// are too small to pay for the table, or whose owner list exceeds the table, are batched
-// and searched in global memory as before.
+// with enough work, N+(x) is loaded once into a shared-memory hash table and the block's 8
+// warps split the segment's items evenly; each probe is then a quarter of a coalesced
+// 16-byte N+(y) load plus ~1 shared-memory access instead of a log2(d+(x)) chain of L1
+// loads. Hub owners whose list exceeds the table (d+ > kSupCap) run several passes, one per
+// kSupCap-key slice of the sorted N+(x); a pass skips the elements outside its key range.
+// Segments too small to pay for the table are batched and searched in global memory.
 #ifndef TDG_SUP_TAB
-#define TDG_SUP_TAB 4096  // shared-memory table slots (4 B key + 2 B position): owners with d+ <= 3/4 TAB
+#define TDG_SUP_TAB 4096  // shared-memory table slots (4 B key + 2 B position + 2 B counter)
 #endif
 constexpr uint32_t kSupTab = TDG_SUP_TAB;
+constexpr uint32_t kSupCap = 3 * kSupTab / 4;  // keys per table at the full-size load of 3/4
 #ifndef TDG_SUP_LOAD
 #define TDG_SUP_LOAD 4  // table slots per key when the table is not full size (C5: 2 -> 4: 1089 -> 1047 ms)
 #endif
-constexpr size_t kSupSmem = size_t(kSupTab) * (sizeof(uint32_t) + sizeof(uint16_t));
-static_assert(kSupTab % 4 == 0 && 3 * kSupTab / 4 < 65536, "bucketed owner table: u16 positions");
+constexpr size_t kSupSmem = size_t(kSupTab) * (sizeof(uint32_t) + 2 * sizeof(uint16_t));
+static_assert(kSupTab % 4 == 0 && kSupCap < 65536, "bucketed owner table: u16 positions and counters");
 #ifndef TDG_SUP_SEGMIN
 #define TDG_SUP_SEGMIN 512u  // a segment gets a table if its probes * SEGDIV >= max(d+(x), SEGMIN)
 #endif
@@ -130,7 +140,7 @@ static_assert(kSupTab % 4 == 0 && 3 * kSupTab / 4 < 65536, "bucketed owner table
 #define TDG_SUP_SEGDIV 1u
 #endif
 #ifndef TDG_SUP_MINB
-#define TDG_SUP_MINB 5  // 5 blocks/SM (shared memory allows 5; C5 support 1.39 -> 1.20 s)
+#define TDG_SUP_MINB 4  // 64 registers: the 8-probe-per-lane quad step needs them (C5: MINB 5 797 ms, 4 774 ms, 3 878 ms)
 #endif
 constexpr uint32_t kSupWarps = kThreads / 32;
 
@@ -143,46 +153,71 @@ __device__ __forceinline__ uint32_t tab_hash(uint32_t c, uint32_t mask) {
 
 // Owner table in shared memory, BUCKETED: 4-key buckets (one 16-byte LDS.128 compares four
 // keys), linear probing over buckets, keys claimed in slot order inside a bucket (so a
-// bucket whose last slot is empty ends a miss); the position of the key in N+(x) sits in a
-// parallel u16 array, read only on a hit. (The previous 8-byte (key, position) slots with
-// per-slot probing took ~3-8 dependent shared loads per miss at the 3/4 load of the
-// d+ > 1024 owners that carry ~70 % of C5's probes.)
+// bucket whose last slot is empty ends a miss). A hit bumps the slot's 16-bit counter
+// (packed pairs, one 32-bit shared-memory atomic; a slot is hit at most once per task of the
+// segment, <= d+(x) < 2^16 times); the counters are flushed to s through the slots' u16
+// positions in N+(x) once per segment, so a triangle costs one global atomic, not two.
+template <bool kRange>
 struct SupportTabPolicy {
     const DevGraph& g;
     uint32_t* s;
     const uint32_t* elems;
     const uint4* keys4;      // nb buckets of 4 keys
-    const uint16_t* pos;     // 4 * nb positions
+    uint32_t* cnt2;          // 2 * nb words: u16 hit counters of the 4 * nb slots
     uint32_t bmask;          // nb - 1
+    uint32_t kmin, kmax;     // key range of this pass (kRange)
     static constexpr bool kFast = true;
+    static constexpr bool kRunForm = true;
     static constexpr int kUnroll = TDG_SUP_U;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
-    __device__ uint32_t find(const ITask&, uint32_t c) const {
-        uint32_t b = tab_hash(c, bmask);
+    // slot of key c or kNone, given its home bucket's key vector
+    __device__ __forceinline__ uint32_t slot_of(uint32_t c, uint32_t b, uint4 kv) const {
         while (true) {
-            const uint4 v = keys4[b];
-            const uint32_t k = v.x == c ? 0u : v.y == c ? 1u : v.z == c ? 2u : v.w == c ? 3u : 4u;
-            if (k < 4u) return pos[4u * b + k];
-            if (v.w == kHEmpty) return kNone;
+            const uint32_t k = kv.x == c ? 0u : kv.y == c ? 1u : kv.z == c ? 2u : kv.w == c ? 3u : 4u;
+            if (k < 4u) return 4u * b + k;
+            if (kv.w == kHEmpty) return kNone;
             b = (b + 1) & bmask;
+            kv = keys4[b];
         }
     }
-    // U items per lane per engine step: the U list loads and lookups issue together and
-    // the engine's per-step bookkeeping is amortised over 32U probes.
     template <int U>
     __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
-        uint32_t c[U], p[U];
+        uint4 v[U];
+        uint32_t base[U];
 #pragma unroll
         for (int q = 0; q < U; q++) {
-            TDG_CHECK(!act[q] || uint64_t(ko[q].oa) + ja[q] < g.m);
-            c[q] = act[q] ? elems[ko[q].oa + ja[q]] : 0u;
+            base[q] = (ko[q].oa & ~3u) + 4u * ja[q];
+            TDG_CHECK(!act[q] || uint64_t(base[q]) + 3 < uint64_t(g.m) + 4);
+            v[q] = act[q] ? __ldg(reinterpret_cast<const uint4*>(elems + base[q])) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int q = 0; q < U; q++) {
-            p[q] = act[q] ? find(ko[q], c[q]) : kNone;
-            TDG_CHECK(p[q] == kNone || uint64_t(ko[q].ob) + p[q] < g.m);
+            const uint32_t c[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+            const uint32_t ly = ko[q].lb >> 16;
+            uint32_t b[4];
+            uint4 kv[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {  // the four home buckets, loaded together
+                b[e] = tab_hash(c[e], bmask);
+                kv[e] = keys4[b[e]];
+            }
+            uint32_t hq = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const uint32_t idx = base[q] + e;
+                bool ok = act[q] && idx - ko[q].oa < ly;  // (unsigned: also drops idx < oa)
+                if (kRange) ok = ok && c[e] >= kmin && c[e] <= kmax;
+                if (ok) {
+                    const uint32_t sl = slot_of(c[e], b[e], kv[e]);
+                    if (sl != kNone) {
+                        atomicAdd(&s[idx], 1u);
+                        atomicAdd(&cnt2[sl >> 1], 1u << ((sl & 1u) << 4));
+                        hq++;
+                    }
+                }
+            }
+            count_own(s, ko[q].id, hq);
         }
-        visit_all<U>(s, ko, ja, p);
     }
 };
 
@@ -200,18 +235,20 @@ __device__ __forceinline__ uint32_t task_in(unsigned long long x, uint32_t lo, u
 __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
                                                           const unsigned long long* wpre, const unsigned long long* bsum,
                                                           uint32_t nchunks, SupportCtl* ctl) {
-    extern __shared__ uint4 tab_keys4[];  // kSupTab keys, then kSupTab u16 positions
+    extern __shared__ uint4 tab_keys4[];  // kSupTab keys, then kSupTab u16 positions, then kSupTab u16 counters
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     __shared__ uint32_t sh_p;
     const unsigned long long W = chunk_offsets<kThreads>(bsum, nchunks, sboff);
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->probes = W;
     if (W == 0) return;
     const uint32_t m = g.m, CH = chunk_len(m, nchunks);
     const uint32_t wid = threadIdx.x >> 5;
     unsigned long long PS = (W + 4ull * gridDim.x - 1) / (4ull * gridDim.x);
-    PS = PS < 4096 ? 4096 : PS;
+    PS = PS < 1024 ? 1024 : PS;
     const unsigned long long npieces = (W + PS - 1) / PS;
     auto start = [&](uint32_t t) -> unsigned long long { return t < m ? sboff[t / CH] + wpre[t] : W; };
+    uint32_t* keys = reinterpret_cast<uint32_t*>(tab_keys4);
+    uint16_t* tpos = reinterpret_cast<uint16_t*>(keys + kSupTab);
+    uint32_t* cnt2 = reinterpret_cast<uint32_t*>(tpos + kSupTab);
     SupportPolicy SP{g, s, g.oadj};
     while (true) {
         if (threadIdx.x == 0) sh_p = atomicAdd(&ctl->piece_head, 1u);
@@ -233,8 +270,8 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
                 send = start(tend);
                 send = send < x1 ? send : x1;
                 dp = g.opos[x + 1] - g.opos[x];
-                table = 4u * dp <= 3u * kSupTab &&
-                        (send - bend) * TDG_SUP_SEGDIV >= (dp > TDG_SUP_SEGMIN ? dp : TDG_SUP_SEGMIN);
+                // (items are quads: ~4 probes each; a hub pays one pass per kSupCap keys)
+                table = (send - bend) * 4u * TDG_SUP_SEGDIV >= (dp > TDG_SUP_SEGMIN ? dp : TDG_SUP_SEGMIN);
                 if (table) break;
                 bend = send;
                 j = tend;
@@ -247,49 +284,76 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
             }
             if (!table) break;  // bend == x1
             // table segment: owner x, tasks [j, tend), items [bend, send)
-            uint32_t size = 64;
-            while (size < TDG_SUP_LOAD * dp && size < kSupTab) size <<= 1;  // load <= 1/LOAD, or <= 3/4 at full size
-            uint32_t* keys = reinterpret_cast<uint32_t*>(tab_keys4);
-            uint16_t* tpos = reinterpret_cast<uint16_t*>(keys + kSupTab);
-            const uint32_t bmask = size / 4 - 1;
-            for (uint32_t q = threadIdx.x; q < size / 4; q += kThreads)
-                tab_keys4[q] = make_uint4(kHEmpty, kHEmpty, kHEmpty, kHEmpty);
+            const uint32_t o = g.opos[x];
+            const unsigned long long w0 = bend + (send - bend) * wid / kSupWarps;
+            const unsigned long long w1 = bend + (send - bend) * (wid + 1) / kSupWarps;
+            const uint32_t t0 = w0 < w1 ? task_in(w0, j, tend, wpre, sboff, CH) : 0u;
             if (threadIdx.x == 0) {
                 atomicAdd(&ctl->tab_elems, static_cast<unsigned long long>(dp));
                 atomicAdd(&ctl->tab_segments, 1ull);
+                if (dp > kSupCap) atomicAdd(&ctl->hub_items, (send - bend) * ((dp + kSupCap - 1) / kSupCap));
             }
-            __syncthreads();
-            const uint32_t o = g.opos[x];
-            for (uint32_t q = threadIdx.x; q < dp; q += kThreads) {
-                const uint32_t c = g.oadj[o + q];
-                uint32_t b = tab_hash(c, bmask);
-                while (true) {  // first free slot of the bucket (slots fill in order), else the next bucket
-                    uint32_t k = 0;
-                    while (k < 4u && atomicCAS(&keys[4u * b + k], kHEmpty, c) != kHEmpty) k++;
-                    if (k < 4u) {
-                        tpos[4u * b + k] = static_cast<uint16_t>(q);  // position in N+(x), as the search form's find returns
-                        break;
+            for (uint32_t p0 = 0; p0 < dp; p0 += kSupCap) {  // one pass per kSupCap keys of the sorted N+(x)
+                const uint32_t nk = dp - p0 < kSupCap ? dp - p0 : kSupCap;
+                uint32_t size = 64;
+                while (size < TDG_SUP_LOAD * nk && size < kSupTab) size <<= 1;  // load <= 1/LOAD, or <= 3/4 at full size
+                const uint32_t bmask = size / 4 - 1;
+                for (uint32_t q = threadIdx.x; q < size / 4; q += kThreads)
+                    tab_keys4[q] = make_uint4(kHEmpty, kHEmpty, kHEmpty, kHEmpty);
+                for (uint32_t q = threadIdx.x; q < size / 2; q += kThreads) cnt2[q] = 0;
+                __syncthreads();
+                for (uint32_t q = threadIdx.x; q < nk; q += kThreads) {
+                    const uint32_t c = g.oadj[o + p0 + q];
+                    uint32_t b = tab_hash(c, bmask);
+                    while (true) {  // first free slot of the bucket (slots fill in order), else the next bucket
+                        uint32_t k = 0;
+                        while (k < 4u && atomicCAS(&keys[4u * b + k], kHEmpty, c) != kHEmpty) k++;
+                        if (k < 4u) {
+                            tpos[4u * b + k] = static_cast<uint16_t>(q);  // position in this slice of N+(x)
+                            break;
+                        }
+                        b = (b + 1) & bmask;
                     }
-                    b = (b + 1) & bmask;
                 }
+                __syncthreads();
+                if (w0 < w1) {
+                    if (dp > kSupCap) {
+                        SupportTabPolicy<true> TP{g, s, g.oadj, tab_keys4, cnt2, bmask, g.oadj[o + p0], g.oadj[o + p0 + nk - 1]};
+                        run_items(TP, w0, w1, t0, m, wpre, sboff, CH);
+                    } else {
+                        SupportTabPolicy<false> TP{g, s, g.oadj, tab_keys4, cnt2, bmask, 0u, 0u};
+                        run_items(TP, w0, w1, t0, m, wpre, sboff, CH);
+                    }
+                }
+                __syncthreads();
+                // flush the slots' hit counters: s[slot of x -> key] += count
+                for (uint32_t q = threadIdx.x; q < size / 2; q += kThreads) {
+                    const uint32_t c2 = cnt2[q];
+                    if (c2 & 0xffffu) atomicAdd(&s[o + p0 + tpos[2u * q]], c2 & 0xffffu);
+                    if (c2 >> 16) atomicAdd(&s[o + p0 + tpos[2u * q + 1]], c2 >> 16);
+                }
+                __syncthreads();
             }
-            __syncthreads();
-            SupportTabPolicy TP{g, s, g.oadj, tab_keys4, tpos, bmask};
-            const unsigned long long w0 = bend + (send - bend) * wid / kSupWarps;
-            const unsigned long long w1 = bend + (send - bend) * (wid + 1) / kSupWarps;
-            if (w0 < w1) run_items(TP, w0, w1, task_in(w0, j, tend, wpre, sboff, CH), m, wpre, sboff, CH);
-            __syncthreads();
             base = send;
             i = tend;
         }
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_support_prep(DevGraph g, unsigned long long* wpre, unsigned long long* bsum) {
+// Work of task t: the quads of N+(y) (kQuads) or its elements; the element total is the
+// pass's probe count.
+template <bool kQuads>
+__global__ void __launch_bounds__(kThreads) k_support_prep(DevGraph g, unsigned long long* wpre, unsigned long long* bsum,
+                                                           SupportCtl* ctl) {
+    unsigned long long elems = 0;
     prep_items<kThreads>(g.m, [&](uint32_t t) {
         const uint32_t y = g.adj[g.stask[t]];
-        return g.opos[y + 1] - g.opos[y];
+        const uint32_t oa = g.opos[y], len = g.opos[y + 1] - oa;
+        elems += len;
+        return kQuads ? quads_of(oa, len) : len;
     }, wpre, bsum);
+    for (int o = 16; o > 0; o >>= 1) elems += shfl64(elems, lane_id() ^ o);
+    if (lane_id() == 0 && elems) atomicAdd(&ctl->probes, elems);
 }
 
 // triangle_count (triangle.cpp:90-116): the same task stream with no per-edge writes; each
@@ -302,8 +366,9 @@ struct CountPolicy {
     static constexpr int kUnroll = 1;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
     __device__ uint32_t find(const ITask& k, uint32_t x) const {
-        const uint32_t p = lower_bound_u32(g.oadj + k.ob, k.lb, x);
-        return (p < k.lb && g.oadj[k.ob + p] == x) ? p : kNone;
+        const uint32_t lx = k.lb & 0xffffu;
+        const uint32_t p = lower_bound_u32(g.oadj + k.ob, lx, x);
+        return (p < lx && g.oadj[k.ob + p] == x) ? p : kNone;
     }
     __device__ void visit(bool, bool hit, const ITask&, uint32_t, uint32_t) {
         count += static_cast<unsigned long long>(__popc(__ballot_sync(kFull, hit)));
@@ -315,9 +380,8 @@ __global__ void __launch_bounds__(kThreads) k_triangle_count(DevGraph g, const u
                                                              SupportCtl* ctl) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     CountPolicy P{g, g.oadj};
-    const unsigned long long W = process_items<kThreads>(P, g.m, wpre, bsum, nchunks, &ctl->piece_head, sboff);
+    process_items<kThreads>(P, g.m, wpre, bsum, nchunks, &ctl->piece_head, sboff);
     if (lane_id() == 0 && P.count) atomicAdd(&ctl->tri3, P.count);
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->probes = W;
 }
 
 __global__ void __launch_bounds__(kThreads) k_support(DevGraph g, uint32_t* __restrict__ s,
@@ -325,8 +389,7 @@ __global__ void __launch_bounds__(kThreads) k_support(DevGraph g, uint32_t* __re
                                                       uint32_t nchunks, SupportCtl* ctl) {
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     SupportPolicy P{g, s, g.oadj};
-    const unsigned long long W = process_items<kThreads>(P, g.m, wpre, bsum, nchunks, &ctl->piece_head, sboff);
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->probes = W;
+    process_items<kThreads>(P, g.m, wpre, bsum, nchunks, &ctl->piece_head, sboff);
 }
 
 __global__ void k_support_sum(const uint32_t* __restrict__ s, uint32_t m, SupportCtl* ctl) {
@@ -361,7 +424,7 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* w
     if (per_sm < 1) per_sm = 1;
     unsigned grid = static_cast<unsigned>(sm_count * per_sm);
     const unsigned nchunks = grid < kMaxChunks ? grid : kMaxChunks;
-    k_support_prep<<<nchunks, kThreads, 0, st>>>(g, wpre, bsum);
+    k_support_prep<true><<<nchunks, kThreads, 0, st>>>(g, wpre, bsum, ctl);
     static const bool tab_form = [] {
         const char* e = std::getenv("TDG_SUP_FORM");  // diagnostic A/B: "search" = global search only
         return !(e && e[0] == 's');
@@ -392,7 +455,7 @@ cudaError_t launch_triangle_count(const DevGraph& g, unsigned long long* wpre, u
     if (per_sm < 1) per_sm = 1;
     const unsigned grid = static_cast<unsigned>(sm_count * per_sm);
     const unsigned nchunks = grid < kMaxChunks ? grid : kMaxChunks;
-    k_support_prep<<<nchunks, kThreads, 0, st>>>(g, wpre, bsum);
+    k_support_prep<false><<<nchunks, kThreads, 0, st>>>(g, wpre, bsum, ctl);
     k_triangle_count<<<grid, kThreads, 0, st>>>(g, wpre, bsum, nchunks, ctl);
     (*launches) += 2;
     return cudaGetLastError();

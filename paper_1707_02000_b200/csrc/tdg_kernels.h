@@ -68,7 +68,8 @@ struct SupportCtl {
     unsigned long long probes;        // probe items of the support pass
     unsigned long long tab_elems;     // N+(owner) elements loaded into shared-memory tables
     unsigned long long tab_segments;  // owner segments served from a shared-memory table
-    unsigned long long search_items;  // probe items binary-searched in global memory instead
+    unsigned long long search_items;  // work items (16-byte list quads) binary-searched in global memory instead
+    unsigned long long hub_items;     // quads x passes of owners whose N+ exceeds one table (d+ > 3/4 TDG_SUP_TAB)
 };
 constexpr uint32_t kMaxChunks = 1024;  // max blocks of a prep grid (one work chunk each)
 // Requires internal edge ids (launch_internal_ids): s[m] is indexed by oriented slot.

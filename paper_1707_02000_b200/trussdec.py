@@ -212,7 +212,7 @@ class Context:
 
     COUNTER_NAMES = ("filter", "pbits", "walk", "slots", "hits", "dead", "dec", "repair", "next", "cross",
                      "comp_in", "comp_kept", "comp_long", "scan_in", "scan_out", "tasks", "sorted", "marks",
-                     "sup_tab_elems", "sup_segments", "sup_search")
+                     "sup_tab_elems", "sup_segments", "sup_search", "sup_hub")
 
     def counters(self) -> dict:
         """tdg_counters: access tallies of this context's last truss/support call (per-probe
