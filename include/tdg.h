@@ -92,6 +92,8 @@ typedef struct tdg_times {
     uint32_t t_max;     /* max trussness (0 when m == 0)                                  */
     uint32_t kernel_launches; /* kernels this call launched                               */
     double compact_ms;  /*   of process_ms: adjacency compactions (device clock)          */
+    double rebuild_ms;  /*   of process_ms: hash-table rebuilds on the live graph         */
+    uint64_t table_rebuilds; /* hash-table rebuilds executed inside the peel              */
 } tdg_times;
 
 typedef struct tdg_graph_stats {
@@ -219,6 +221,8 @@ enum {
     TDG_CNT_TASKS,          /* peel: sub-level tasks (curr edges at levels > 0)            */
     TDG_CNT_SORTED,         /* peel: tasks bucket-sorted by searched vertex                */
     TDG_CNT_MARKS,          /* peel: processed-bitmap marks                                */
+    TDG_CNT_REBUILD_EDGES,  /* peel: live edges re-inserted by table rebuilds (2 inserts each) */
+    TDG_CNT_REBUILD_BUCKETS,/* peel: table buckets cleared by rebuilds                     */
     TDG_CNT_SUP_TAB_ELEMS,  /* support: N+(owner) elements loaded into shared-memory tables */
     TDG_CNT_SUP_SEGMENTS,   /* support: owner segments served from a shared-memory table   */
     TDG_CNT_SUP_SEARCH,     /* support: 16-byte list quads binary-searched in global memory */

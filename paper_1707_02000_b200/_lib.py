@@ -50,7 +50,8 @@ class tdg_times(C.Structure):
                                           "process_ms", "d2h_ms", "total_ms")] + \
                [(k, C.c_uint64) for k in ("triangles", "support_probes", "levels", "sublevels", "scans", "compactions", "probes", "hits",
                                           "dead_probes")] + \
-               [("t_max", C.c_uint32), ("kernel_launches", C.c_uint32), ("compact_ms", C.c_double)]
+               [("t_max", C.c_uint32), ("kernel_launches", C.c_uint32), ("compact_ms", C.c_double),
+                ("rebuild_ms", C.c_double), ("table_rebuilds", C.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -138,8 +138,7 @@ __global__ void k_hsize(const uint32_t* __restrict__ off, uint32_t n, uint32_t* 
 // Tables of at most kHSmall buckets are built in shared memory, one warp per vertex (up to
 // kHMid, one block per vertex), and written out with coalesced stores (random global CAS
 // inserts were 1.8 % of a C5 step).
-constexpr uint32_t kHSmall = 256;        // buckets (8 KB) per warp
-constexpr uint32_t kHMid = 8 * kHSmall;  // block-built tables use the block's whole 64 KB
+// (kHSmall = 256 buckets, 8 KB, per warp; kHMid = 8 kHSmall: the block's whole 64 KB — tdg_common.cuh)
 
 __global__ void __launch_bounds__(256) k_hbuild_small(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
                                                       const uint32_t* __restrict__ eid, const uint32_t* __restrict__ hbo,

@@ -252,6 +252,20 @@ struct tdg_context {
         p.seid = cscr + word / 2;  // 2 words later (word is in bytes: 2 * word / 4 u32)
         p.desc = reinterpret_cast<uint4*>(cscr);
         p.pbits = pbits.as<uint32_t>();
+        p.hbo_w = hbo.as<uint32_t>();
+        p.htab_w = htab.as<uint32_t>();
+        p.filt_w = peel_filter() ? filt.as<unsigned long long>() : nullptr;
+        p.rebuild_num = kPeelRebuildNum;
+        p.rebuild_den = kPeelRebuildDen;
+        p.nseg = kPeelRebuildMax + 1;
+        if (const char* rb = std::getenv("TDG_REBUILD")) {  // diagnostic: "num/den[/max]", "0/0" = never
+            unsigned a = 0, b = 0, mx = kPeelRebuildMax;
+            if (std::sscanf(rb, "%u/%u/%u", &a, &b, &mx) >= 2) {
+                p.rebuild_num = a;
+                p.rebuild_den = b;
+                p.nseg = (mx < 16 ? mx : 16) + 1;
+            }
+        }
         return p;
     }
     void trim() {
@@ -526,6 +540,8 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
             times->scan_ms = pc.scan_ns * 1e-6;
             times->process_ms = pc.proc_ns * 1e-6;
             times->compact_ms = pc.compact_ns * 1e-6;
+            times->rebuild_ms = pc.rebuild_ns * 1e-6;
+            times->table_rebuilds = pc.table_rebuilds;
             times->probes = pc.probes;
             times->hits = pc.cnt[kCntHits];
             times->dead_probes = pc.cnt[kCntDead];
@@ -1015,6 +1031,7 @@ int tdg_process_sublevel(tdg_context* ctx, const tdg_csr* g, uint32_t* s, uint32
 }
 
 static_assert(int(TDG_CNT_SCAN_IN) == int(kCntScanIn) && int(TDG_CNT_MARKS) == int(kCntMarks) &&
+                  int(TDG_CNT_REBUILD_BUCKETS) == int(kCntRebuildBuckets) &&
                   int(TDG_CNT_COMP_LONG) == int(kCntCompLong) && int(TDG_CNT_SUP_TAB_ELEMS) == int(kPeelCnt),
               "tdg.h counter order must follow PeelCnt");
 

@@ -304,22 +304,19 @@ __device__ unsigned long long process_items(Policy& P, uint32_t ntasks, const un
         unsigned long long S0 = (W + 2ull * nwarps - 1) / (2ull * nwarps);
         S0 = (S0 + kStep - 1) / kStep * kStep;
         const unsigned long long minp = kStep > TDG_MIN_PIECE ? kStep : TDG_MIN_PIECE;
-        // The first piece of every warp is static (piece = warp index, warp 0 of every block
-        // first so a small phase spreads over the SMs); only the pieces after that first tier
-        // are pulled from the counter. A small phase therefore issues no atomics at all (one
-        // same-address atomic per warp was ~5 us of every small sub-level).
-        unsigned long long x0, x1;
-        guided_piece(nwarps, W, nwarps, S0, minp, &x0, &x1);
-        const bool dynamic = x0 < W;
-        uint32_t p = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+        // Every piece is pulled from the counter in arrival order, so concurrently running
+        // warps work on neighbouring stretches of the (sorted) task axis. (A static first tier
+        // — piece = warp index, no atomics in one-tier phases — was measured: C1 peel 16.1 vs
+        // 15.6 ms, C5 2.66 vs 2.40 s; removed.)
         while (true) {
+            uint32_t p = 0;
+            if (lane == 0) p = atomicAdd(piece_head, 1u);
+            p = __shfl_sync(kFull, p, 0);
+            unsigned long long x0, x1;
             guided_piece(p, W, nwarps, S0, minp, &x0, &x1);
             if (x0 >= W) break;
             run_items(P, x0, x1, task_at(x0, ntasks, wpre, sboff, nchunks, CH), ntasks, wpre, sboff, CH);
             if constexpr (has_flush<Policy>::value) P.flush();
-            if (!dynamic) break;
-            if (lane == 0) p = nwarps + atomicAdd(piece_head, 1u);
-            p = __shfl_sync(kFull, p, 0);
         }
         return W;
     }

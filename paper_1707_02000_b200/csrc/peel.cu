@@ -65,6 +65,38 @@ constexpr int kWarps = kPeelThreads / 32;
 #ifndef TDG_HTAB_NC
 #define TDG_HTAB_NC 0  // table slots through the read-only (non-coherent) path: tables never change in the peel
 #endif
+#ifndef TDG_FILT_NC
+#define TDG_FILT_NC 0  // filter words through the read-only path
+#endif
+// Cold phases (rebuild, compaction, bucket sort) can be kept out of line so that they do not
+// take part in the register allocation of the probe loop.
+#ifndef TDG_NOINLINE_RB
+#define TDG_NOINLINE_RB 0
+#endif
+#ifndef TDG_NOINLINE_COLD
+#define TDG_NOINLINE_COLD 0
+#endif
+#if TDG_NOINLINE_RB
+#define TDG_COLD_RB __device__ __noinline__
+#else
+#define TDG_COLD_RB __device__
+#endif
+#if TDG_NOINLINE_COLD
+#define TDG_COLD __device__ __noinline__
+#else
+#define TDG_COLD __device__
+#endif
+// The process phase out of line: the probe loop gets a register allocation of its own; the
+// level loop's state is saved around the call (once per sub-level) instead of being spilled
+// and refilled inside the loop.
+#ifndef TDG_NOINLINE_HOT
+#define TDG_NOINLINE_HOT 0
+#endif
+#if TDG_NOINLINE_HOT
+#define TDG_HOT __device__ __noinline__
+#else
+#define TDG_HOT __device__
+#endif
 #ifndef TDG_PEEL_FAST
 #define TDG_PEEL_FAST 0  // engine fast path (intersect.cuh) for the peel's probe loop
 #endif
@@ -156,7 +188,7 @@ __device__ __forceinline__ void emit_many(const uint32_t (&o)[N], uint32_t* ctr,
 #ifndef TDG_PEEL_QUEUE
 #define TDG_PEEL_QUEUE 1
 #endif
-constexpr int kQB = 3;                       // candidates per lane per drain
+constexpr int kQB = TDG_PEEL_U > 3 ? TDG_PEEL_U : 3;  // candidates per lane per drain
 constexpr uint32_t kQBatch = 32u * kQB;      // drain size
 constexpr uint32_t kQCap = 2u * kQBatch;     // < kQBatch left + <= 32 * TDG_PEEL_U new (<= kQBatch)
 static_assert(32 * TDG_PEEL_U <= int(kQBatch), "one engine step must fit behind a partial batch");
@@ -362,7 +394,7 @@ struct PeelPolicy {
             if constexpr (kCount) cn[kCntPbits] += (pbits && look[q]) ? 1u : 0u;
             fw[q] = ~0ull;
             if (g.filt && look[q] && ko[q].lb >= kFMin) {
-                fw[q] = __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q]));
+                fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q])) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q])];
                 if constexpr (kCount) cn[kCntFilter]++;
             }
         }
@@ -436,7 +468,7 @@ struct PeelPolicy {
             for (int q = 0; q < U; q++) {
                 fw[q] = ~0ull;
                 if (look[q] && ko[q].lb >= kFMin) {
-                    fw[q] = __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q]));
+                    fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q])) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q])];
                     if constexpr (kCount) cn[kCntFilter]++;
                 }
             }
@@ -634,7 +666,7 @@ __device__ __forceinline__ uint32_t bucket_add(uint32_t* ctr, uint32_t bucket, b
     return pos;
 }
 
-__device__ void phase_bucket_hist(const DevGraph& g, const uint32_t* curr, uint32_t cs, uint32_t* hist, uint32_t shift) {
+TDG_COLD void phase_bucket_hist(const DevGraph& g, const uint32_t* curr, uint32_t cs, uint32_t* hist, uint32_t shift) {
     for (uint64_t i0 = uint64_t(blockIdx.x) * kPeelThreads + (threadIdx.x & ~31u); i0 < cs;
          i0 += uint64_t(gridDim.x) * kPeelThreads) {
         const uint64_t i = i0 + lane_id();
@@ -645,7 +677,7 @@ __device__ void phase_bucket_hist(const DevGraph& g, const uint32_t* curr, uint3
 }
 
 // One block: cursor = exclusive scan of hist; hist is cleared for the next use.
-__device__ void phase_bucket_scan(uint32_t* hist, uint32_t* cursor) {
+TDG_COLD void phase_bucket_scan(uint32_t* hist, uint32_t* cursor) {
     constexpr uint32_t per = kBuckets / kPeelThreads;
     const uint32_t c0 = threadIdx.x * per;
     unsigned long long loc = 0;
@@ -660,7 +692,7 @@ __device__ void phase_bucket_scan(uint32_t* hist, uint32_t* cursor) {
     }
 }
 
-__device__ void phase_bucket_scatter(const DevGraph& g, const uint32_t* curr, uint32_t cs, uint32_t* cursor,
+TDG_COLD void phase_bucket_scatter(const DevGraph& g, const uint32_t* curr, uint32_t cs, uint32_t* cursor,
                                      uint32_t shift, uint32_t* out) {
     for (uint64_t i0 = uint64_t(blockIdx.x) * kPeelThreads + (threadIdx.x & ~31u); i0 < cs;
          i0 += uint64_t(gridDim.x) * kPeelThreads) {
@@ -714,7 +746,7 @@ __device__ __forceinline__ PeelShared& peel_shared() {
 
 // process_sublevel (truss_parallel.cpp:39-104) for curr[0..cs) on the intersection engine.
 template <bool kCount>
-__device__ unsigned long long phase_process(const DevGraph& g, unsigned long long* ss, uint32_t level,
+TDG_HOT unsigned long long phase_process(const DevGraph& g, unsigned long long* ss, uint32_t level,
                                             uint32_t K, const uint32_t* curr, uint32_t cs,
                                             const unsigned long long* wpre, const unsigned long long* bsum,
                                             uint32_t nchunks, PhaseCtr* ph, uint32_t* next,
@@ -730,8 +762,7 @@ __device__ unsigned long long phase_process(const DevGraph& g, unsigned long lon
 // and process as ONE phase: every block resolves all task descriptors itself (one task per
 // thread) into shared memory and scans their probe counts there, then runs the usual
 // process phase on that one-chunk prefix — no work-prefix round trip through global memory,
-// one grid barrier per sub-level instead of two (and no piece-counter atomics: the first
-// tier of pieces is static). Same probes, same sets.
+// one grid barrier per sub-level instead of two. Same probes, same sets.
 #ifndef TDG_FUSE_MAX
 #define TDG_FUSE_MAX 256
 #endif
@@ -784,7 +815,7 @@ constexpr int kCompactU = 4;  // entries per lane per compaction round
 __device__ __forceinline__ bool long_list(const DevGraph& g, uint32_t u) { return g.off[u + 1] - g.off[u] > kBigList; }
 
 template <bool kCount>
-__device__ void phase_compact_long(const DevGraph& g, const PeelBufs& pb, uint32_t nchunks) {
+TDG_COLD void phase_compact_long(const DevGraph& g, const PeelBufs& pb, uint32_t nchunks) {
     const uint32_t lane = lane_id();
     const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
     for (uint32_t c = gw; c < nchunks; c += nw) {
@@ -832,7 +863,7 @@ __device__ void phase_compact_long(const DevGraph& g, const PeelBufs& pb, uint32
     }
 }
 
-__device__ void phase_compact_copy(const DevGraph& g, const PeelBufs& pb, uint32_t nchunks) {
+TDG_COLD void phase_compact_copy(const DevGraph& g, const PeelBufs& pb, uint32_t nchunks) {
     const uint32_t lane = lane_id();
     const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
     for (uint32_t c = gw; c < nchunks; c += nw) {
@@ -861,7 +892,7 @@ __device__ void phase_compact_copy(const DevGraph& g, const PeelBufs& pb, uint32
 // its list's kept count before this round (per-vertex counter in shared memory) plus the
 // kept entries before it in the round.
 template <bool kCount>
-__device__ void phase_compact_short(const DevGraph& g, const uint32_t* pbits, unsigned long long* cnt) {
+TDG_COLD void phase_compact_short(const DevGraph& g, const uint32_t* pbits, unsigned long long* cnt) {
     __shared__ uint32_t sh_kept[kWarps][32];
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     const uint32_t gw = (blockIdx.x * kPeelThreads + threadIdx.x) >> 5, nw = (gridDim.x * kPeelThreads) >> 5;
@@ -976,7 +1007,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
     GridBar grid{cg::this_grid(), &pb.ctl->bar, 0u};
     PeelCtl* ctl = pb.ctl;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m;
+    uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m, live_at_rebuild = g.m;
     uint32_t B = 0, fi = 1, nF = 0, xp = 0;  // near bound, far list parity/size, crosser parity
     const uint32_t* pend = nullptr;          // last sub-level's curr, not yet in pbits
     uint32_t pend_n = 0;
@@ -984,7 +1015,20 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
     unsigned long long t_prev = leader ? gtimer() : 0;
     unsigned long long sub_w = 0;
     const uint32_t nchunks = vload(&ctl->nchunks);
+    bool resumed = pb.seg > 0;
+    uint32_t cs = 0;
+    if (resumed) {  // a later segment of the same decomposition: continue where the last one left
+        if (vload(&ctl->done)) return;
+        const PeelResume& rs = ctl->rs;
+        j = rs.j; level = rs.level; K = rs.K; nA = rs.nA; ai = rs.ai; li = rs.li;
+        live_at_compact = rs.live_at_compact; live_at_rebuild = rs.live_at_rebuild;
+        B = rs.B; fi = rs.fi; nF = rs.nF; xp = rs.xp; cs = rs.cs;
+        grid.target = rs.bar_target;
+        implicit = false;
+        if (leader) ctl->rebuild_ns += t_prev - rs.t_exit;
+    }
     while (true) {
+        if (!resumed) {
         // ---- scan at `level` (one grid barrier); re-split the far list once level >= B
         const bool resplit = implicit || level >= B;
         // (crossers sit right after the near list, in the same buffer: A[ai][nA .. nA + nX))
@@ -1007,7 +1051,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         if (leader) { const unsigned long long t = gtimer(); ctl->scan_ns += t - t_prev; t_prev = t; }
         j++;
         const PhaseCtr* r = &ctl->ph[(j - 1) % 3];
-        uint32_t cs = vload(&r->out_size);
+        cs = vload(&r->out_size);
         nA = vload(&r->alive_size);
         const uint32_t mins = vload(&r->min_s);
         ai ^= 1;
@@ -1037,10 +1081,30 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             grid.sync();
             phase_compact_copy(g, pb, nchunks);
             grid.sync();
-            if (leader) { const unsigned long long t = gtimer(); ctl->compact_ns += t - t_prev; }
+            unsigned long long t_c = 0;
+            if (leader) { t_c = gtimer(); ctl->compact_ns += t_c - t_prev; }
             j++;
             live_at_compact = static_cast<uint32_t>(live);
+            // ---- table rebuild on the live graph (kernels below): leave the launch here; the
+            // host has queued the rebuild kernels and the next segment, which resumes at the
+            // sub-levels of this level
+            if (kPeelRebuildDen && pb.seg + 1 < pb.nseg && pb.rebuild_den &&
+                live * pb.rebuild_den <= static_cast<unsigned long long>(live_at_rebuild) * pb.rebuild_num) {
+                if (leader) {
+                    PeelResume& rs = ctl->rs;
+                    rs.j = j; rs.level = level; rs.K = K; rs.nA = nA; rs.ai = ai; rs.li = li;
+                    rs.live_at_compact = live_at_compact; rs.live_at_rebuild = static_cast<uint32_t>(live);
+                    rs.B = B; rs.fi = fi; rs.nF = nF; rs.xp = xp; rs.cs = cs;
+                    rs.bar_target = grid.target;
+                    rs.t_exit = t_c;
+                    ctl->table_rebuilds++;
+                    ctl->cnt[kCntRebuildEdges] += live;
+                }
+                return;
+            }
         }
+        }  // !resumed
+        resumed = false;
         // ---- sub-levels: prep + process (two grid barriers each; level 0 one)
         while (true) {
             if (leader) {
@@ -1110,7 +1174,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             }
             j++;
             K++;
-            r = &ctl->ph[(j - 1) % 3];
+            const PhaseCtr* r = &ctl->ph[(j - 1) % 3];
             pend = pb.L[li];
             pend_n = cs;
             cs = vload(&r->out_size);
@@ -1119,7 +1183,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         }
         level++;
     }
-    if (leader) ctl->final_stamp = K;
+    if (leader) { ctl->final_stamp = K; ctl->done = 1; }
 #if TDG_DIAG_RATIO
     if (leader) {
         printf("DIAG ratio lb/la (<2,<4,<8,<16,<64,>=64):");
@@ -1130,6 +1194,145 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
         for (int i = 0; i < 16; i++) d_diag[i] = 0;
     }
 #endif
+}
+
+// ---- table rebuild on the live graph. The tables and filters are built for the input
+// graph, but most of the peel's probes run when only a fraction of the edges is left (C5: 2/3
+// of the probes with < 1/4 of the edges live), and their random accesses keep spreading over
+// the full-size tables (16.7 GB + 0.75 GB of filters at C5). Right after a compaction (dl =
+// live degree of every vertex, pbits = the processed edges) k_peel ends its segment; these
+// kernels re-size the tables to the live degrees and refill them with the live edges only,
+// in place, and the next segment resumes: the working set shrinks with the graph (filters
+// become L2-resident), dead peers vanish from the tables. Same layout and lookup as the build
+// (tdg_common.cuh); values carry no orientation bit (the peel ignores it). The kernels are
+// queued with the segments and do nothing once the level loop has finished. (Run inside the
+// cooperative kernel instead, the same phases cost the probe loop ~10 % through its register
+// allocation.)
+constexpr unsigned kRbBlocks = 592;
+static_assert(kRbBlocks <= kMaxChunks, "one vertex chunk per block");
+
+// Pass 1: block b owns vertex chunk b: hbo[x] = chunk-local exclusive prefix of nb(x) =
+// hbuckets(dl[x]); bsum[b] = the chunk's bucket count.
+__global__ void __launch_bounds__(kPeelThreads) k_rb_sizes(DevGraph g, PeelBufs pb) {
+    if (pb.ctl->done) return;
+    const uint32_t CH = chunk_len(g.n, gridDim.x);
+    const uint64_t lo = uint64_t(blockIdx.x) * CH;
+    const uint64_t hi = lo + CH < g.n ? lo + CH : g.n;
+    unsigned long long run = 0;
+    for (uint64_t x0 = lo; x0 < hi; x0 += kPeelThreads) {
+        const uint64_t x = x0 + threadIdx.x;
+        const unsigned long long nb = x < hi ? hbuckets(g.dl[x]) : 0u;
+        unsigned long long tot;
+        const unsigned long long ex = block_excl_scan64<kPeelThreads>(nb, tot);
+        if (x < hi) pb.hbo_w[x] = static_cast<uint32_t>(run + ex);
+        run += tot;
+    }
+    if (threadIdx.x == 0) pb.bsum[blockIdx.x] = run;
+}
+
+// Pass 2: chunk offsets added to the chunk-local prefixes; the new tables' buckets and filter
+// words cleared.
+__global__ void __launch_bounds__(kPeelThreads) k_rb_clear(DevGraph g, PeelBufs pb) {
+    if (pb.ctl->done) return;
+    __shared__ unsigned long long sboff[kMaxChunks + 1];
+    const unsigned long long total = chunk_offsets<kPeelThreads>(pb.bsum, gridDim.x, sboff);
+    const uint32_t CH = chunk_len(g.n, gridDim.x);
+    const uint64_t lo = uint64_t(blockIdx.x) * CH;
+    const uint64_t hi = lo + CH < g.n ? lo + CH : g.n;
+    const uint32_t add = static_cast<uint32_t>(sboff[blockIdx.x]);
+    for (uint64_t x = lo + threadIdx.x; x < hi; x += kPeelThreads) pb.hbo_w[x] += add;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        pb.hbo_w[g.n] = static_cast<uint32_t>(total);
+        pb.ctl->cnt[kCntRebuildBuckets] += total;
+    }
+    TDG_CHECK(total <= g.nbuckets);
+    uint4* t4 = reinterpret_cast<uint4*>(pb.htab_w);
+    const uint4 e4 = make_uint4(kHEmpty, kHEmpty, kHEmpty, kHEmpty);
+    const uint64_t stride = uint64_t(gridDim.x) * kPeelThreads, tid = uint64_t(blockIdx.x) * kPeelThreads + threadIdx.x;
+    for (uint64_t i = tid; i < 2 * total; i += stride) t4[i] = e4;
+    if (pb.filt_w) {
+        const uint64_t fw = (total >> kFShift) + 1;
+        for (uint64_t i = tid; i < fw; i += stride) pb.filt_w[i] = 0ull;
+    }
+}
+
+// Pass 3a: tables of at most kHMid buckets, from the live lists (adj / eid [off[x], +dl[x])),
+// in shared memory — one warp per table up to kHSmall buckets, the block for the rest — and
+// written out with coalesced stores (as k_hbuild_small, build.cu).
+__global__ void __launch_bounds__(256) k_rb_small(DevGraph g, PeelBufs pb) {
+    if (pb.ctl->done) return;
+    extern __shared__ uint32_t rb_smem[];  // 8 warps x kHSmall buckets x 8 words
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    uint32_t* t = rb_smem + w * kHSmall * 8u;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    // a warp scans 32 vertices at a time and builds the non-empty small tables among them
+    for (uint64_t x0 = uint64_t((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; x0 < g.n; x0 += uint64_t(nw) * 32) {
+        const uint64_t xl = x0 + lane;
+        uint32_t nbl = 0;
+        if (xl < g.n) nbl = pb.hbo_w[xl + 1] - pb.hbo_w[xl];
+        uint32_t todo = __ballot_sync(kFull, nbl != 0 && nbl <= kHSmall);
+        while (todo) {
+            const uint32_t src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t x = static_cast<uint32_t>(x0) + src;
+            const uint32_t nb = __shfl_sync(kFull, nbl, src);
+            const uint32_t b0 = pb.hbo_w[x];
+            for (uint32_t i = lane; i < 8u * nb; i += 32) t[i] = kHEmpty;
+            __syncwarp();
+            const uint32_t o = g.off[x], d = g.dl[x];
+            for (uint32_t i = lane; i < d; i += 32) bucket_insert(t, nb, g.adj[o + i], g.eid[o + i]);
+            __syncwarp();
+            uint32_t* gt = pb.htab_w + 8ull * b0;
+            for (uint32_t i = lane; i < 8u * nb; i += 32) gt[i] = t[i];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    __shared__ uint32_t q[256];
+    __shared__ uint32_t qn;
+    for (uint64_t c0 = uint64_t(blockIdx.x) * 256; c0 < g.n; c0 += uint64_t(gridDim.x) * 256) {
+        if (threadIdx.x == 0) qn = 0;
+        __syncthreads();
+        const uint64_t x = c0 + threadIdx.x;
+        if (x < g.n) {
+            const uint32_t nb = pb.hbo_w[x + 1] - pb.hbo_w[x];
+            if (nb > kHSmall && nb <= kHMid) q[atomicAdd(&qn, 1u)] = static_cast<uint32_t>(x);
+        }
+        __syncthreads();
+        const uint32_t cnt = qn;
+        for (uint32_t k = 0; k < cnt; k++) {
+            const uint32_t v = q[k], b0 = pb.hbo_w[v], nb = pb.hbo_w[v + 1] - b0, o = g.off[v], d = g.dl[v];
+            for (uint32_t i = threadIdx.x; i < 8u * nb; i += blockDim.x) rb_smem[i] = kHEmpty;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) bucket_insert(rb_smem, nb, g.adj[o + i], g.eid[o + i]);
+            __syncthreads();
+            uint32_t* gt = pb.htab_w + 8ull * b0;
+            for (uint32_t i = threadIdx.x; i < 8u * nb; i += blockDim.x) gt[i] = rb_smem[i];
+            __syncthreads();
+        }
+    }
+}
+
+// Pass 3b: every live edge e = {u, v} (processed bit clear) enters the tables of more than
+// kHMid buckets among its endpoints' (global CAS) and the filters of those with a filter.
+// Internal edge ids follow the oriented lists, so consecutive edges share u.
+__global__ void __launch_bounds__(256) k_rb_big(DevGraph g, PeelBufs pb) {
+    if (pb.ctl->done) return;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t e0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; e0 < g.m; e0 += stride) {
+        const uint32_t w = pb.pbits[e0 >> 5];
+        const uint64_t e = e0 + lane_id();
+        if (e >= g.m || ((w >> lane_id()) & 1u)) continue;
+        const uint2 p = g.el[e];
+#pragma unroll
+        for (int side = 0; side < 2; side++) {
+            const uint32_t x = side ? p.y : p.x, y = side ? p.x : p.y;
+            const uint32_t b0 = pb.hbo_w[x], nb = pb.hbo_w[x + 1] - b0;
+            TDG_CHECK(nb > 0 && uint64_t(b0) + nb <= g.nbuckets);
+            if (nb > kHMid) bucket_insert(pb.htab_w + 8ull * b0, nb, y, static_cast<uint32_t>(e));
+            if (pb.filt_w && nb >= kFMin) atomicOr(&pb.filt_w[fword_index(b0, nb, y)], fbits(hmix(y)));
+        }
+    }
 }
 
 __global__ void k_peel_init(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ dl,
@@ -1242,15 +1445,34 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
-    unsigned na = 0;
-    at[na].id = cudaLaunchAttributeCooperative;
-    at[na].val.cooperative = 1;
-    na++;
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = na;
-    err = cudaLaunchKernelExC(&cfg, kern, args);
-    (*launches) += 2;
-    return err;
+    cfg.numAttrs = 1;
+    // Segments: the level loop leaves its launch where the tables are to be rebuilt on the
+    // live graph (at most kPeelRebuildMax times); the rebuild kernels and the next segment are
+    // queued up front and do nothing once the loop has finished — no host round trip.
+    const bool rebuild = kPeelRebuildDen != 0 && p.rebuild_den != 0 && p.hbo_w && p.htab_w;
+    pp.nseg = rebuild && p.nseg > 1 ? p.nseg : 1;
+    const size_t rb_smem = 8u * kHSmall * 8u * sizeof(uint32_t);
+    if (rebuild) {
+        err = cudaFuncSetAttribute(k_rb_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rb_smem));
+        if (err != cudaSuccess) return err;
+    }
+    (*launches)++;  // k_peel_init
+    for (uint32_t seg = 0; seg < pp.nseg; seg++) {
+        pp.seg = seg;
+        if ((err = cudaLaunchKernelExC(&cfg, kern, args)) != cudaSuccess) return err;
+        (*launches)++;
+        if (seg + 1 < pp.nseg) {
+            k_rb_sizes<<<kRbBlocks, kPeelThreads, 0, st>>>(gg, pp);
+            k_rb_clear<<<kRbBlocks, kPeelThreads, 0, st>>>(gg, pp);
+            k_rb_small<<<148u * 3u, 256, rb_smem, st>>>(gg, pp);
+            k_rb_big<<<148u * 16u, 256, 0, st>>>(gg, pp);
+            (*launches) += 4;
+        }
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const unsigned long long* ss, const uint32_t* oeid, uint32_t m, uint32_t* truss, PeelCtl* ctl,

@@ -179,6 +179,11 @@ __device__ __forceinline__ void bucket_insert(uint32_t* t, uint32_t nb, uint32_t
     }
 }
 
+// Table sizes (buckets) up to which a table is built in shared memory by one warp / one
+// block and written out with coalesced stores (build.cu, and the peel's rebuilds).
+constexpr uint32_t kHSmall = 256;        // buckets (8 KB) per warp
+constexpr uint32_t kHMid = 8 * kHSmall;  // block-built tables use the block's whole 64 KB
+
 // ---- per-vertex membership filters (register-blocked Bloom filters) in front of the big
 // tables (nb >= kFMin buckets). Vertex x owns the 64-bit words [hbo[x] >> kFShift,
 // hbo[x+1] >> kFShift) — disjoint ranges, 2^kFShift buckets (~2^(kFShift+2) / kHF keys) per

@@ -177,10 +177,18 @@ enum PeelCnt : int {
     kCntTasks,       // sub-level tasks prepped (level > 0)
     kCntSorted,      // tasks bucket-sorted by searched vertex
     kCntMarks,       // processed-bitmap marks (one per curr edge)
+    kCntRebuildEdges,    // live edges re-inserted by table rebuilds (two inserts each)
+    kCntRebuildBuckets,  // table buckets cleared by rebuilds
     kPeelCnt
 };
 constexpr int kCntFirstPhase = kCntScanIn;
 
+// Level-loop state carried from one k_peel segment to the next (a segment ends where the
+// tables are rebuilt on the live graph, peel.cu).
+struct PeelResume {
+    uint32_t j, level, K, nA, ai, li, live_at_compact, live_at_rebuild, B, fi, nF, xp, cs, bar_target;
+    unsigned long long t_exit;  // device clock when the segment ended
+};
 struct PeelCtl {
     PhaseCtr ph[3];
     uint32_t levels_len;   // last non-empty level + 1
@@ -200,6 +208,10 @@ struct PeelCtl {
     uint32_t xcnt[2];  // crosser-list append counters (peel.cu near/far scan)
     uint32_t rebuilds;  // scans that re-split the far list
     uint32_t bar;       // grid-barrier arrival counter (TDG_FAST_BARRIER)
+    uint32_t table_rebuilds;        // hash-table rebuilds on the live graph
+    uint32_t done;                  // the level loop has finished (later segments are no-ops)
+    unsigned long long rebuild_ns;  // device-clock time in table rebuilds
+    PeelResume rs;
 };
 struct PeelBufs {
     uint32_t* s;               // support (u32): input of the peel / step-function I/O
@@ -228,9 +240,27 @@ struct PeelBufs {
     uint32_t* F[2];   // m each: far live edges (support >= the near bound when split)
     // (far edges whose support crossed below the near bound are appended right after the
     // current near list A[ai], which the next scan reads as one list)
+    // writable views of the graph's tables for the in-peel rebuild on the live graph (the
+    // DevGraph pointers are the same arrays, read-only for the probes)
+    uint32_t* hbo_w;
+    uint32_t* htab_w;
+    unsigned long long* filt_w;
+    uint32_t rebuild_num, rebuild_den;  // rebuild once live <= num/den of the last (re)build (den 0: never)
+    uint32_t seg, nseg;                 // this k_peel launch is segment seg of at most nseg
     uint4* desc;      // m: per-sub-level task descriptors (aliases the compaction scratch; a
                       // bucket-sorted curr list follows the descriptors)
 };
+// In-peel table rebuild (peel.cu): once live edges <= NUM/DEN of those at the last (re)build.
+#ifndef TDG_REBUILD_NUM
+#define TDG_REBUILD_NUM 1
+#endif
+#ifndef TDG_REBUILD_DEN
+#define TDG_REBUILD_DEN 4  // 0 = never (compiled out)
+#endif
+#ifndef TDG_REBUILD_MAX
+#define TDG_REBUILD_MAX 3  // at most this many rebuilds per decomposition (k_peel segments - 1)
+#endif
+constexpr uint32_t kPeelRebuildNum = TDG_REBUILD_NUM, kPeelRebuildDen = TDG_REBUILD_DEN, kPeelRebuildMax = TDG_REBUILD_MAX;
 #ifndef TDG_BUCKET_BITS
 #define TDG_BUCKET_BITS 16
 #endif

@@ -212,6 +212,7 @@ class Context:
 
     COUNTER_NAMES = ("filter", "pbits", "walk", "slots", "hits", "dead", "dec", "repair", "next", "cross",
                      "comp_in", "comp_kept", "comp_long", "scan_in", "scan_out", "tasks", "sorted", "marks",
+                     "rebuild_edges", "rebuild_buckets",
                      "sup_tab_elems", "sup_segments", "sup_search", "sup_hub")
 
     def counters(self) -> dict:

@@ -23,7 +23,7 @@ for _ in range(reps):
     truss, nsl, _, t = ctx.truss(g)
     ok = hashlib.sha256(np.ascontiguousarray(truss, np.uint32).tobytes()).hexdigest() == gold.get("truss_sha") \
         and nsl == gold.get("nsl")
-    keep = ("build_ms", "support_ms", "peel_ms", "scan_ms", "process_ms", "compact_ms", "total_ms", "probes",
+    keep = ("build_ms", "support_ms", "peel_ms", "scan_ms", "process_ms", "compact_ms", "rebuild_ms", "table_rebuilds", "total_ms", "probes",
             "support_probes", "sublevels")
     print(f"C{cfg} m={m} wall={time.time()-t0:.3f}s parity={'ok' if ok else 'FAIL'} lib={os.path.relpath(_lib.TDG_SO, ROOT)}",
           {k: round(v, 2) if isinstance(v, float) else v for k, v in t.items() if k in keep}, flush=True)
