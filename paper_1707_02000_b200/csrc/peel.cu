@@ -198,7 +198,7 @@ static_assert(32 * TDG_PEEL_U <= int(kQBatch), "one engine step must fit behind 
 // endpoint's hash table (whose value is the other peer's id). kCount = the diagnostic
 // instantiation that also tallies every access class of the probe (PeelCnt, for the byte
 // model of bench.py); the timed path is the kCount = false instantiation.
-template <bool kCount>
+template <bool kCount, uint32_t kShift = kFShift>
 struct PeelPolicy {
     const DevGraph& g;
     unsigned long long* ss;
@@ -394,7 +394,7 @@ struct PeelPolicy {
             if constexpr (kCount) cn[kCntPbits] += (pbits && look[q]) ? 1u : 0u;
             fw[q] = ~0ull;
             if (g.filt && look[q] && ko[q].lb >= kFMin) {
-                fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q])) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q])];
+                fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift)];
                 if constexpr (kCount) cn[kCntFilter]++;
             }
         }
@@ -468,7 +468,7 @@ struct PeelPolicy {
             for (int q = 0; q < U; q++) {
                 fw[q] = ~0ull;
                 if (look[q] && ko[q].lb >= kFMin) {
-                    fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q])) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q])];
+                    fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift)];
                     if constexpr (kCount) cn[kCntFilter]++;
                 }
             }
@@ -745,7 +745,7 @@ __device__ __forceinline__ PeelShared& peel_shared() {
 }
 
 // process_sublevel (truss_parallel.cpp:39-104) for curr[0..cs) on the intersection engine.
-template <bool kCount>
+template <bool kCount, uint32_t kShift = kFShift>
 TDG_HOT unsigned long long phase_process(const DevGraph& g, unsigned long long* ss, uint32_t level,
                                             uint32_t K, const uint32_t* curr, uint32_t cs,
                                             const unsigned long long* wpre, const unsigned long long* bsum,
@@ -753,7 +753,7 @@ TDG_HOT unsigned long long phase_process(const DevGraph& g, unsigned long long* 
                                             unsigned long long* cnt, uint32_t B, uint32_t* X, uint32_t* xcnt,
                                             const uint32_t* pbits, const uint4* desc) {
     PeelShared& sh = peel_shared();
-    PeelPolicy<kCount> P{g, ss, level, K, curr, ph, next, g.adj, cnt, B, X, xcnt, pbits, desc,
+    PeelPolicy<kCount, kShift> P{g, ss, level, K, curr, ph, next, g.adj, cnt, B, X, xcnt, pbits, desc,
                          sh.squeue + (TDG_PEEL_QUEUE ? (threadIdx.x >> 5) * 5 * kQCap : 0)};
     return process_items<kPeelThreads>(P, cs, wpre, bsum, nchunks, &ph->piece_head, sh.sboff);
 }
@@ -1002,21 +1002,26 @@ struct GridBar {
 };
 
 // The whole truss_parallel level loop (truss_parallel.cpp:119-144) in one launch.
-template <bool kCount>
+// kShift: filter density of the tables this segment probes (the input graph's, or the rebuilt).
+template <bool kCount, uint32_t kShift>
 __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g, PeelBufs pb) {
     GridBar grid{cg::this_grid(), &pb.ctl->bar, 0u};
     PeelCtl* ctl = pb.ctl;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
-    uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m, live_at_rebuild = g.m;
-    uint32_t B = 0, fi = 1, nF = 0, xp = 0;  // near bound, far list parity/size, crosser parity
-    const uint32_t* pend = nullptr;          // last sub-level's curr, not yet in pbits
-    uint32_t pend_n = 0;
-    bool implicit = true;
-    unsigned long long t_prev = leader ? gtimer() : 0;
-    unsigned long long sub_w = 0;
+    // The level loop's state is volatile ON PURPOSE: it then lives in the thread's stack frame
+    // (L1-resident local memory, a few accesses per phase) and never competes with the probe
+    // loop for registers. Left to the register allocator, small changes to this loop moved
+    // spills into the probe loop and cost up to 15 % of the peel (64 registers per thread).
+    volatile uint32_t j = 0, level = 0, K = 1, nA = g.m, ai = 0, li = 0, live_at_compact = g.m, live_at_rebuild = g.m;
+    volatile uint32_t B = 0, fi = 1, nF = 0, xp = 0;  // near bound, far list parity/size, crosser parity
+    const uint32_t* volatile pend = nullptr;          // last sub-level's curr, not yet in pbits
+    volatile uint32_t pend_n = 0;
+    volatile bool implicit = true;
+    volatile unsigned long long t_prev = leader ? gtimer() : 0;
+    volatile unsigned long long sub_w = 0;
     const uint32_t nchunks = vload(&ctl->nchunks);
-    bool resumed = pb.seg > 0;
-    uint32_t cs = 0;
+    volatile bool resumed = pb.seg > 0;
+    volatile uint32_t cs = 0;
     if (resumed) {  // a later segment of the same decomposition: continue where the last one left
         if (vload(&ctl->done)) return;
         const PeelResume& rs = ctl->rs;
@@ -1088,8 +1093,12 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
             // ---- table rebuild on the live graph (kernels below): leave the launch here; the
             // host has queued the rebuild kernels and the next segment, which resumes at the
             // sub-levels of this level
+            // (the denser rebuilt filters must fit the words allocated for the input graph's:
+            // the live tables have at most kHF * live / 2 + min(n, 2 live) buckets)
+            const unsigned long long nb_max = kHF * live / 2 + (2 * live < g.n ? 2 * live : g.n);
             if (kPeelRebuildDen && pb.seg + 1 < pb.nseg && pb.rebuild_den &&
-                live * pb.rebuild_den <= static_cast<unsigned long long>(live_at_rebuild) * pb.rebuild_num) {
+                live * pb.rebuild_den <= static_cast<unsigned long long>(live_at_rebuild) * pb.rebuild_num &&
+                (nb_max >> kFShiftRebuild) + 1 <= (g.nbuckets >> kFShift)) {
                 if (leader) {
                     PeelResume& rs = ctl->rs;
                     rs.j = j; rs.level = level; rs.K = K; rs.nA = nA; rs.ai = ai; rs.li = li;
@@ -1151,7 +1160,7 @@ __global__ void __launch_bounds__(kPeelThreads, TDG_PEEL_MINB) k_peel(DevGraph g
                     grid.sync();
                 }
                 const unsigned long long W =
-                    phase_process<kCount>(g, pb.ss, level, K, tasks, cs, wp, bs, nch, &ctl->ph[j % 3], pb.L[li ^ 1],
+                    phase_process<kCount, kShift>(g, pb.ss, level, K, tasks, cs, wp, bs, nch, &ctl->ph[j % 3], pb.L[li ^ 1],
                                           ctl->cnt, B, pb.A[ai] + nA, &ctl->xcnt[xp], pb.pbits, dsc);
                 if (leader) {
                     ctl->probes += W;
@@ -1251,7 +1260,7 @@ __global__ void __launch_bounds__(kPeelThreads) k_rb_clear(DevGraph g, PeelBufs 
     const uint64_t stride = uint64_t(gridDim.x) * kPeelThreads, tid = uint64_t(blockIdx.x) * kPeelThreads + threadIdx.x;
     for (uint64_t i = tid; i < 2 * total; i += stride) t4[i] = e4;
     if (pb.filt_w) {
-        const uint64_t fw = (total >> kFShift) + 1;
+        const uint64_t fw = (total >> kFShiftRebuild) + 1;
         for (uint64_t i = tid; i < fw; i += stride) pb.filt_w[i] = 0ull;
     }
 }
@@ -1330,7 +1339,7 @@ __global__ void __launch_bounds__(256) k_rb_big(DevGraph g, PeelBufs pb) {
             const uint32_t b0 = pb.hbo_w[x], nb = pb.hbo_w[x + 1] - b0;
             TDG_CHECK(nb > 0 && uint64_t(b0) + nb <= g.nbuckets);
             if (nb > kHMid) bucket_insert(pb.htab_w + 8ull * b0, nb, y, static_cast<uint32_t>(e));
-            if (pb.filt_w && nb >= kFMin) atomicOr(&pb.filt_w[fword_index(b0, nb, y)], fbits(hmix(y)));
+            if (pb.filt_w && nb >= kFMin) atomicOr(&pb.filt_w[fword_index(b0, nb, y, kFShiftRebuild)], fbits(hmix(y)));
         }
     }
 }
@@ -1425,8 +1434,13 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     if (g.m == 0) return cudaSuccess;
     if (p.pbits && (err = cudaMemsetAsync(p.pbits, 0, size_t((g.m + 31) / 32) * 4, st)) != cudaSuccess) return err;
     k_peel_init<<<148 * 4, 256, 0, st>>>(g.off, g.n, g.dl, p.s, g.m, p.ss, p.ctl, p.chunks, p.chunk_cap);
-    // count mode (diagnostic, PeelBufs::count): the instantiation that tallies every access
-    const void* kern = p.count ? reinterpret_cast<const void*>(k_peel<true>) : reinterpret_cast<const void*>(k_peel<false>);
+    // count mode (diagnostic, PeelBufs::count): the instantiation that tallies every access;
+    // segments after a rebuild probe the denser rebuilt filters (a second instantiation: a
+    // run-time shift in the probe loop cost 15 % through its register allocation)
+    const void* kern = p.count ? reinterpret_cast<const void*>(k_peel<true, kFShift>)
+                               : reinterpret_cast<const void*>(k_peel<false, kFShift>);
+    const void* kern_rb = p.count ? reinterpret_cast<const void*>(k_peel<true, kFShiftRebuild>)
+                                  : reinterpret_cast<const void*>(k_peel<false, kFShiftRebuild>);
     int per_sm = 0;
     err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPeelThreads, 0);
     if (err != cudaSuccess) return err;
@@ -1462,7 +1476,7 @@ cudaError_t launch_peel(const DevGraph& g, const PeelBufs& p, int sm_count, cuda
     (*launches)++;  // k_peel_init
     for (uint32_t seg = 0; seg < pp.nseg; seg++) {
         pp.seg = seg;
-        if ((err = cudaLaunchKernelExC(&cfg, kern, args)) != cudaSuccess) return err;
+        if ((err = cudaLaunchKernelExC(&cfg, seg ? kern_rb : kern, args)) != cudaSuccess) return err;
         (*launches)++;
         if (seg + 1 < pp.nseg) {
             k_rb_sizes<<<kRbBlocks, kPeelThreads, 0, st>>>(gg, pp);

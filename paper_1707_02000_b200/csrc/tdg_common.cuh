@@ -191,7 +191,7 @@ constexpr uint32_t kHMid = 8 * kHSmall;  // block-built tables use the block's w
 // whose bits are not all set is a certain miss and skips the table walk, so the misses of a
 // sub-level (~3/4 of all probes) mostly hit the L2-resident filters instead of DRAM.
 #ifndef TDG_FMIN
-#define TDG_FMIN 256  // buckets (1024 slots)
+#define TDG_FMIN 64  // buckets (256 slots; C5 peel 2150 -> 2127 ms against 256)
 #endif
 constexpr uint32_t kFMin = TDG_FMIN;
 #ifndef TDG_FSHIFT
@@ -201,6 +201,11 @@ constexpr uint32_t kFMin = TDG_FMIN;
 #define TDG_FK 3  // bits set per key
 #endif
 constexpr uint32_t kFShift = TDG_FSHIFT;
+#ifndef TDG_FSHIFT_REBUILD
+#define TDG_FSHIFT_REBUILD 2  // filters of the tables rebuilt on the live graph: 8 bits per key
+#endif
+constexpr uint32_t kFShiftRebuild = TDG_FSHIFT_REBUILD;
+static_assert(kFShiftRebuild <= kFShift, "rebuilt filters may be denser, never sparser (TDG_FMIN covers both)");
 static_assert((kFMin >> kFShift) >= 1, "every filtered vertex owns at least one filter word");
 
 __device__ __forceinline__ uint32_t fword(uint32_t x) {
@@ -217,8 +222,10 @@ __device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(k
 }
 
 // Filter word of key y in the filter of a vertex whose table is buckets [ob, ob + nb).
-__device__ __forceinline__ uint64_t fword_index(uint32_t ob, uint32_t nb, uint32_t y) {
-    const uint32_t f0 = ob >> kFShift, f1 = (ob + nb) >> kFShift;
+// (fshift: kFShift for the tables of the input graph; the peel's rebuilds on the live graph
+// use the denser kFShiftRebuild — a template parameter of the k_peel segments.)
+__device__ __forceinline__ uint64_t fword_index(uint32_t ob, uint32_t nb, uint32_t y, uint32_t fshift = kFShift) {
+    const uint32_t f0 = ob >> fshift, f1 = (ob + nb) >> fshift;
     return static_cast<uint64_t>(f0) + __umulhi(fword(y), f1 - f0);
 }
 
