@@ -132,6 +132,16 @@ int tdg_truss_device(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out,
 int tdg_support(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times);
 int tdg_support_device(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out,
                        tdg_times* times);
+/* Sharded support pass (the reference has no distributed code — this is the
+ * multi-GPU form of support_am4, proj/src/triangle.cpp:26-61). Every rank holds the whole
+ * graph; shard `shard` of `nshards` counts only the triangles found in its equal-work stretch
+ * of the probe axis and writes PARTIAL supports (support_out[m], host / device, reference
+ * edge ids). The element-wise sum over all shards (one all-reduce of m u32) is exactly
+ * support_am4's result; there is no other exchange. */
+int tdg_support_shard(tdg_context* ctx, const tdg_csr* g, uint32_t shard, uint32_t nshards,
+                      uint32_t* support_out, tdg_times* times);
+int tdg_support_shard_device(tdg_context* ctx, const tdg_csr* g, uint32_t shard,
+                             uint32_t nshards, uint32_t* support_out, tdg_times* times);
 
 /* build_truss_graph: eo[n], eid[2m], el[2m] (el[2e], el[2e+1] = u < v). Host pointers. */
 int tdg_build_truss_graph(tdg_context* ctx, const tdg_csr* g, uint32_t* eo, uint32_t* eid,

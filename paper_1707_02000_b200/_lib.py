@@ -81,6 +81,8 @@ SIGNATURES = [
     ("tdg_counters", _i32, [_vp, _P(_u64), _u64]),
     ("tdg_support", _i32, [_vp, _P(tdg_csr), _vp, _P(tdg_times)]),
     ("tdg_support_device", _i32, [_vp, _P(tdg_csr), _vp, _P(tdg_times)]),
+    ("tdg_support_shard", _i32, [_vp, _P(tdg_csr), _u32, _u32, _vp, _P(tdg_times)]),
+    ("tdg_support_shard_device", _i32, [_vp, _P(tdg_csr), _u32, _u32, _vp, _P(tdg_times)]),
     ("tdg_build_truss_graph", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp]),
     ("tdg_stats", _i32, [_vp, _P(tdg_csr), _P(tdg_graph_stats)]),
     ("tdg_triangle_count", _i32, [_vp, _P(tdg_csr), _P(_u64), _P(tdg_times)]),

@@ -550,10 +550,12 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
     });
 }
 
-int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times, bool host) {
+int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times, bool host,
+                 uint32_t shard = 0, uint32_t nshards = 1) {
     return guarded([&] {
         tdg_context* c = resolve(ctx);
         c->use();
+        if (nshards == 0 || shard >= nshards) throw Fail{TDG_ERR_INVALID, "shard must be < nshards"};
         const Dims d = check_graph(g, host);
         if (!support_out && d.m) throw Fail{TDG_ERR_INVALID, "support_out is NULL"};
         c->launches = 0;
@@ -562,7 +564,7 @@ int support_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_
         uint32_t* sdev = support_out;
         if (host) { c->sup.ensure(size_t(d.m) * 4 + 4, "support copy"); sdev = c->sup.as<uint32_t>(); }
         ck(launch_support(dg, c->s, c->wpre, c->bsum.as<unsigned long long>(),
-                          c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches), "support kernels");
+                          c->sctl.as<SupportCtl>(), c->sms, c->stream, &c->launches, shard, nshards), "support kernels");
         ck(launch_to_ref(dg.oeid, c->s, d.m, 0, sdev, c->stream, &c->launches), "support to ref ids");
         ck(cudaEventRecord(c->ev[3], c->stream), "event");
         if (host && d.m)
@@ -632,6 +634,16 @@ int tdg_support(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_t
 
 int tdg_support_device(tdg_context* ctx, const tdg_csr* g, uint32_t* support_out, tdg_times* times) {
     return support_impl(ctx, g, support_out, times, false);
+}
+
+int tdg_support_shard(tdg_context* ctx, const tdg_csr* g, uint32_t shard, uint32_t nshards, uint32_t* support_out,
+                      tdg_times* times) {
+    return support_impl(ctx, g, support_out, times, true, shard, nshards);
+}
+
+int tdg_support_shard_device(tdg_context* ctx, const tdg_csr* g, uint32_t shard, uint32_t nshards,
+                             uint32_t* support_out, tdg_times* times) {
+    return support_impl(ctx, g, support_out, times, false, shard, nshards);
 }
 
 int tdg_build_truss_graph(tdg_context* ctx, const tdg_csr* g, uint32_t* eo, uint32_t* eid, uint32_t* el) {

@@ -234,17 +234,24 @@ __device__ __forceinline__ uint32_t task_in(unsigned long long x, uint32_t lo, u
 
 __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
                                                           const unsigned long long* wpre, const unsigned long long* bsum,
-                                                          uint32_t nchunks, SupportCtl* ctl) {
+                                                          uint32_t nchunks, SupportCtl* ctl, uint32_t shard,
+                                                          uint32_t nshards) {
     extern __shared__ uint4 tab_keys4[];  // kSupTab keys, then kSupTab u16 positions, then kSupTab u16 counters
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     __shared__ uint32_t sh_p;
     const unsigned long long W = chunk_offsets<kThreads>(bsum, nchunks, sboff);
     if (W == 0) return;
+    // Shard `shard` of `nshards` (the support pass shards with no exchange but a
+    // final sum) owns the contiguous stretch [Wlo, Whi) of the work axis: equal probe work per
+    // shard whatever the degree skew; a shard boundary cuts a task like a piece boundary does.
+    const unsigned long long Wlo = W / nshards * shard + W % nshards * shard / nshards;
+    const unsigned long long Whi = W / nshards * (shard + 1) + W % nshards * (shard + 1) / nshards;
+    if (Whi == Wlo) return;
     const uint32_t m = g.m, CH = chunk_len(m, nchunks);
     const uint32_t wid = threadIdx.x >> 5;
-    unsigned long long PS = (W + 4ull * gridDim.x - 1) / (4ull * gridDim.x);
+    unsigned long long PS = (Whi - Wlo + 4ull * gridDim.x - 1) / (4ull * gridDim.x);
     PS = PS < 1024 ? 1024 : PS;
-    const unsigned long long npieces = (W + PS - 1) / PS;
+    const unsigned long long npieces = (Whi - Wlo + PS - 1) / PS;
     auto start = [&](uint32_t t) -> unsigned long long { return t < m ? sboff[t / CH] + wpre[t] : W; };
     uint32_t* keys = reinterpret_cast<uint32_t*>(tab_keys4);
     uint16_t* tpos = reinterpret_cast<uint16_t*>(keys + kSupTab);
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
         const uint32_t p = sh_p;
         __syncthreads();
         if (p >= npieces) break;
-        const unsigned long long x0 = p * PS, x1 = x0 + PS < W ? x0 + PS : W;
+        const unsigned long long x0 = Wlo + p * PS, x1 = x0 + PS < Whi ? x0 + PS : Whi;
         uint32_t i = task_at(x0, m, wpre, sboff, nchunks, CH);
         unsigned long long base = x0;
         while (base < x1) {
@@ -414,7 +421,8 @@ __global__ void k_support_sum(const uint32_t* __restrict__ s, uint32_t m, Suppor
 
 cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* wpre,
                            unsigned long long* bsum, SupportCtl* ctl, int sm_count, cudaStream_t st,
-                           uint32_t* launches) {
+                           uint32_t* launches, uint32_t shard, uint32_t nshards) {
+    if (nshards == 0 || shard >= nshards) return cudaErrorInvalidValue;
     cudaError_t err = cudaMemsetAsync(ctl, 0, sizeof(SupportCtl), st);
     if (err != cudaSuccess) return err;
     if (g.m == 0) return cudaSuccess;
@@ -437,8 +445,10 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* w
         int tb = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb, k_support_tab, kThreads, smem);
         if (tb < 1) tb = 1;
-        k_support_tab<<<static_cast<unsigned>(sm_count * tb), kThreads, smem, st>>>(g, s, wpre, bsum, nchunks, ctl);
+        k_support_tab<<<static_cast<unsigned>(sm_count * tb), kThreads, smem, st>>>(g, s, wpre, bsum, nchunks, ctl, shard,
+                                                                                    nshards);
     } else {
+        if (nshards != 1) return cudaErrorNotSupported;  // the diagnostic search form is unsharded
         k_support<<<grid, kThreads, 0, st>>>(g, s, wpre, bsum, nchunks, ctl);
     }
     k_support_sum<<<grid, kThreads, 0, st>>>(s, g.m, ctl);

@@ -73,10 +73,11 @@ struct SupportCtl {
 };
 constexpr uint32_t kMaxChunks = 1024;  // max blocks of a prep grid (one work chunk each)
 // Requires internal edge ids (launch_internal_ids): s[m] is indexed by oriented slot.
-// wpre: >= m u64 scratch; bsum: kMaxChunks u64.
+// wpre: >= m u64 scratch; bsum: kMaxChunks u64. shard / nshards: only the triangles found in
+// shard's stretch of the probe axis are counted (the shards' results sum to the supports).
 cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* wpre,
                            unsigned long long* bsum, SupportCtl* ctl, int sm_count, cudaStream_t st,
-                           uint32_t* launches);
+                           uint32_t* launches, uint32_t shard = 0, uint32_t nshards = 1);
 
 // triangle_count (triangle.cpp:90-116): count lands in ctl->tri3 (= T, not 3T).
 cudaError_t launch_triangle_count(const DevGraph& g, unsigned long long* wpre, unsigned long long* bsum,

@@ -262,6 +262,22 @@ class Context:
         _ck(_lib.tdg().tdg_support(self._h, C.byref(v), s.ctypes.data, C.byref(t)))
         return s[: g.m], t.as_dict()
 
+    def support_shard(self, g: CsrGraph, shard: int, nshards: int):
+        """Partial supports of one shard (tdg_support_shard): the shards' arrays sum to support()."""
+        s = np.zeros(max(g.m, 1), np.uint32)
+        t = tdg_times()
+        v = g._view()
+        _ck(_lib.tdg().tdg_support_shard(self._h, C.byref(v), shard, nshards, s.ctypes.data, C.byref(t)))
+        return s[: g.m], t.as_dict()
+
+    def support_shard_device(self, n: int, m: int, off_ptr: int, nb_ptr: int, shard: int, nshards: int,
+                             support_ptr: int) -> dict:
+        """tdg_support_shard_device on device buffers (partial supports stay in HBM for the all-reduce)."""
+        t = tdg_times()
+        v = tdg_csr(n, m, off_ptr, nb_ptr)
+        _ck(_lib.tdg().tdg_support_shard_device(self._h, C.byref(v), shard, nshards, support_ptr, C.byref(t)))
+        return t.as_dict()
+
     def build_truss_graph(self, g: CsrGraph) -> TrussGraph:
         eo = np.zeros(max(g.n, 1), np.uint32)
         eid = np.zeros(max(2 * g.m, 1), np.uint32)
@@ -315,6 +331,50 @@ def triangle_count(tg: TrussGraph | CsrGraph, workers: int = 1) -> int:
 def support_am4(tg: TrussGraph | CsrGraph, workers: int = 1) -> np.ndarray:
     g = tg.csr if isinstance(tg, TrussGraph) else tg
     return default_context().support(g)[0]
+
+
+def allreduce_partial_supports(partial, group=None):
+    """Sum the shards' partial supports over the process group, in place (the one exchange of
+    the sharded support pass). `partial` is a torch tensor of m 32-bit words (on
+    the GPU under NCCL, on the host under gloo) or a numpy uint32 array (gloo). Sums are taken
+    on the int32 view: two's-complement addition is the same bits as uint32 addition."""
+    import torch
+    import torch.distributed as dist
+
+    if isinstance(partial, np.ndarray):
+        t = torch.from_numpy(partial.view(np.int32))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return partial
+    t = partial.view(torch.int32) if partial.dtype != torch.int32 else partial
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return partial
+
+
+def support_am4_sharded(tg: TrussGraph | CsrGraph, group=None, ctx: Context | None = None) -> np.ndarray:
+    """support_am4 (triangle.cpp:26-61) over the ranks of a torch.distributed group: every
+    rank holds the graph, counts the triangles of its equal-work shard on its own GPU and the
+    partial supports are summed with ONE all-reduce of m u32 (NCCL: device buffers; gloo: host).
+    Every rank returns the full support array."""
+    import torch
+    import torch.distributed as dist
+
+    g = tg.csr if isinstance(tg, TrussGraph) else tg
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ctx = ctx or default_context()
+    if dist.get_backend(group) == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
+        off = torch.from_numpy(np.ascontiguousarray(g.offsets, np.int64)).to(dev)
+        nb = torch.from_numpy(np.ascontiguousarray(g.neighbors, np.int32)).to(dev)
+        part = torch.zeros(max(g.m, 1), dtype=torch.int32, device=dev)
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        try:
+            ctx.support_shard_device(g.n, g.m, off.data_ptr(), nb.data_ptr(), rank, world, part.data_ptr())
+        finally:
+            ctx.set_stream(None)
+        allreduce_partial_supports(part, group)
+        return part[: g.m].cpu().numpy().view(np.uint32)
+    part = ctx.support_shard(g, rank, world)[0]
+    return allreduce_partial_supports(np.ascontiguousarray(part), group)
 
 
 def truss_parallel(tg: TrussGraph | CsrGraph, workers: int = 1) -> ParallelDecomposition:

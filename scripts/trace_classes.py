@@ -19,3 +19,12 @@ top = sorted(rows, key=lambda r: -r[3])[:12]
 print("top sub-levels (level, tasks, probes, ms, Gprobes/s):")
 for r in top:
     print("  ", r[0], r[1], r[2], round(r[3] / 1e6, 2), round(r[2] / max(r[3], 1), 1))
+# fused sub-levels (<= 256 tasks) by probe count W
+print("fused sub-levels by probes:")
+print("| probes W | sub-levels | time (ms) | us per sub-level |")
+print("|---|---|---|---|")
+for lo, hi in [(0, 1), (1, 768), (768, 3072), (3072, 12288), (12288, 49152), (49152, 1 << 62)]:
+    rs = [r for r in rows if r[1] <= 256 and lo <= r[2] < hi]
+    if rs:
+        ns = sum(r[3] for r in rs)
+        print(f"| {lo}-{hi} | {len(rs)} | {ns/1e6:.2f} | {ns/1e3/len(rs):.1f} |")

@@ -95,3 +95,44 @@ def test_ncu_traffic_is_tied_to_the_sources(tmp_path, monkeypatch):
     assert bench.ncu_traffic(5).get("stale") is True
     f.write_text(json.dumps({"src_sha": bench.src_sha(), "C5": {"k_peel": {"dram_bytes": 1}}}))
     assert bench.ncu_traffic(5) == {"k_peel": {"dram_bytes": 1}}
+
+
+def _shard_worker(rank, world, port, q):
+    """Rank `rank` of the sharded support pass's host side over gloo: the partial supports
+    (here: the oracle's supports split between the ranks edge by edge, standing in for the GPU
+    shards) are summed by allreduce_partial_supports; every rank must end with the full array."""
+    import numpy as np
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import Oracle
+    from paper_1707_02000_b200 import trussdec
+    orc = Oracle()
+    csr = orc.rmat_graph(9, 8, 11)
+    full = np.asarray(orc.support_am4(csr), np.uint32)
+    rng = np.random.default_rng(5)  # same stream on both ranks
+    cut = (rng.random(len(full)) * (full + 1)).astype(np.uint32)  # 0 <= cut <= full
+    part = cut if rank == 0 else full - cut
+    # wrap-around is part of the contract (u32 sums on the i32 view): plant one
+    part = part.copy()
+    part[0] = np.uint32(0xFFFFFFF0) if rank == 0 else np.uint32(full[0] + 0x10)
+    out = trussdec.allreduce_partial_supports(np.ascontiguousarray(part))
+    q.put((rank, bool(np.array_equal(out, full)), int(full.sum())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_support_allreduce():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[1] for r in res] == [True, True]
+    assert res[0][2] == res[1][2] > 0
