@@ -164,21 +164,27 @@ struct SupportTabPolicy {
     const uint32_t* elems;
     const uint4* keys4;      // nb buckets of 4 keys
     uint32_t* cnt2;          // 2 * nb words: u16 hit counters of the 4 * nb slots
+    uint32_t cnt2_saddr;     // cnt2 as a shared-window address (for red.shared)
     uint32_t bmask;          // nb - 1
     uint32_t kmin, kmax;     // key range of this pass (kRange)
     static constexpr bool kFast = true;
     static constexpr bool kRunForm = true;
     static constexpr int kUnroll = TDG_SUP_U;
     __device__ ITask load(uint32_t t) const { return otask(g, t); }
-    // slot of key c or kNone, given its home bucket's key vector
-    __device__ __forceinline__ uint32_t slot_of(uint32_t c, uint32_t b, uint4 kv) const {
-        while (true) {
-            const uint32_t k = kv.x == c ? 0u : kv.y == c ? 1u : kv.z == c ? 2u : kv.w == c ? 3u : 4u;
-            if (k < 4u) return 4u * b + k;
-            if (kv.w == kHEmpty) return kNone;
-            b = (b + 1) & bmask;
-            kv = keys4[b];
-        }
+    // One-hot match mask of key c in a bucket's key vector (keys are unique: at most one bit).
+    // Four compares folded into a mask: no early-exit branch chain (lanes stay converged).
+    static __device__ __forceinline__ uint32_t onehot(const uint4& kv, uint32_t c) {
+        return (kv.x == c ? 1u : 0u) | (kv.y == c ? 2u : 0u) | (kv.z == c ? 4u : 0u) | (kv.w == c ? 8u : 0u);
+    }
+    // The two counts of a hit as PREDICATED reductions (no divergent branch around them): the
+    // probe-side edge's global counter and the owner-side slot's shared-memory u16 counter.
+    static __device__ __forceinline__ void count_hit(bool hit, uint32_t* gs, uint32_t saddr, uint32_t sval) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+            "@p red.global.add.u32 [%1], 1;\n\t"
+            "@p red.shared.add.u32 [%2], %3;\n\t}"
+            ::"r"(static_cast<uint32_t>(hit)), "l"(gs), "r"(saddr), "r"(sval)
+            : "memory");
     }
     template <int U>
     __device__ void run(const bool (&act)[U], const ITask (&ko)[U], const uint32_t (&ja)[U]) const {
@@ -207,14 +213,19 @@ struct SupportTabPolicy {
                 const uint32_t idx = base[q] + e;
                 bool ok = act[q] && idx - ko[q].oa < ly;  // (unsigned: also drops idx < oa)
                 if (kRange) ok = ok && c[e] >= kmin && c[e] <= kmax;
-                if (ok) {
-                    const uint32_t sl = slot_of(c[e], b[e], kv[e]);
-                    if (sl != kNone) {
-                        atomicAdd(&s[idx], 1u);
-                        atomicAdd(&cnt2[sl >> 1], 1u << ((sl & 1u) << 4));
-                        hq++;
-                    }
+                uint32_t oh = onehot(kv[e], c[e]), bb = b[e];
+                if (ok && oh == 0u && kv[e].w != kHEmpty) {  // home bucket full (rare at load <= 1/4): walk on
+                    uint4 k2;
+                    do {
+                        bb = (bb + 1) & bmask;
+                        k2 = keys4[bb];
+                        oh = onehot(k2, c[e]);
+                    } while (oh == 0u && k2.w != kHEmpty);
                 }
+                const bool hit = ok && oh != 0u;
+                const uint32_t sl = 4u * bb + ((__ffs(oh) - 1) & 3u);  // slot of the match (any in-table value if !hit)
+                count_hit(hit, &s[idx], cnt2_saddr + ((sl >> 1) << 2), 1u << ((sl & 1u) << 4));
+                hq += hit ? 1u : 0u;
             }
             count_own(s, ko[q].id, hq);
         }
@@ -256,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
     uint32_t* keys = reinterpret_cast<uint32_t*>(tab_keys4);
     uint16_t* tpos = reinterpret_cast<uint16_t*>(keys + kSupTab);
     uint32_t* cnt2 = reinterpret_cast<uint32_t*>(tpos + kSupTab);
+    const uint32_t cnt2_saddr = static_cast<uint32_t>(__cvta_generic_to_shared(cnt2));
     SupportPolicy SP{g, s, g.oadj};
     while (true) {
         if (threadIdx.x == 0) sh_p = atomicAdd(&ctl->piece_head, 1u);
@@ -325,10 +337,10 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
                 __syncthreads();
                 if (w0 < w1) {
                     if (dp > kSupCap) {
-                        SupportTabPolicy<true> TP{g, s, g.oadj, tab_keys4, cnt2, bmask, g.oadj[o + p0], g.oadj[o + p0 + nk - 1]};
+                        SupportTabPolicy<true> TP{g, s, g.oadj, tab_keys4, cnt2, cnt2_saddr, bmask, g.oadj[o + p0], g.oadj[o + p0 + nk - 1]};
                         run_items(TP, w0, w1, t0, m, wpre, sboff, CH);
                     } else {
-                        SupportTabPolicy<false> TP{g, s, g.oadj, tab_keys4, cnt2, bmask, 0u, 0u};
+                        SupportTabPolicy<false> TP{g, s, g.oadj, tab_keys4, cnt2, cnt2_saddr, bmask, 0u, 0u};
                         run_items(TP, w0, w1, t0, m, wpre, sboff, CH);
                     }
                 }
