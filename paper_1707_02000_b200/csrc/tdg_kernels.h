@@ -259,7 +259,7 @@ struct PeelBufs {
 #define TDG_REBUILD_DEN 2  // 0 = never (compiled out)
 #endif
 #ifndef TDG_REBUILD_MAX
-#define TDG_REBUILD_MAX 4  // at most this many rebuilds per decomposition (k_peel segments - 1)
+#define TDG_REBUILD_MAX 6  // at most this many rebuilds per decomposition (k_peel segments - 1)
 #endif
 constexpr uint32_t kPeelRebuildNum = TDG_REBUILD_NUM, kPeelRebuildDen = TDG_REBUILD_DEN, kPeelRebuildMax = TDG_REBUILD_MAX;
 #ifndef TDG_BUCKET_BITS
