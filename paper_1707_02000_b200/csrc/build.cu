@@ -207,14 +207,15 @@ __global__ void k_hinsert(const uint32_t* __restrict__ off, const uint32_t* __re
 
 // Filter bits of every slot (x -> y) whose owner table is big enough (tdg_common.cuh).
 __global__ void k_finsert(const uint32_t* __restrict__ hbo, const uint32_t* __restrict__ adj,
-                          const uint32_t* __restrict__ src, uint64_t slots, unsigned long long* __restrict__ filt) {
+                          const uint32_t* __restrict__ src, uint64_t slots, unsigned long long* __restrict__ filt,
+                          uint32_t fscale) {
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t x = src[j];
         const uint32_t b0 = hbo[x], nb = hbo[x + 1] - b0;
         if (nb < kFMin) continue;
         const uint32_t y = adj[j];
-        atomicOr(&filt[fword_index(b0, nb, y)], fbits(hmix(y)));
+        atomicOr(&filt[fword_index(b0, nb, y, kFShift, fscale)], fbits(hmix(y)));
     }
 }
 
@@ -425,7 +426,7 @@ cudaError_t launch_filter_fill(const uint32_t* hbo, const uint32_t* adj, const u
     if (err != cudaSuccess) return err;
     const uint64_t slots = 2ull * m;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
-    k_finsert<<<gs, kThreads, 0, st>>>(hbo, adj, src, slots, filt);
+    k_finsert<<<gs, kThreads, 0, st>>>(hbo, adj, src, slots, filt, filter_scale(n));
     (*launches)++;
     return cudaGetLastError();
 }

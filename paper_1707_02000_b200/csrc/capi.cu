@@ -212,6 +212,7 @@ struct tdg_context {
         g.hbo = hbo.as<uint32_t>();
         g.nbuckets = htab.cap / 32;
         g.filt = peel_filter() ? filt.as<unsigned long long>() : nullptr;
+        g.fscale = filter_scale(n);
         return g;
     }
     PeelBufs peel_bufs(uint32_t n) const {

@@ -394,7 +394,7 @@ struct PeelPolicy {
             if constexpr (kCount) cn[kCntPbits] += (pbits && look[q]) ? 1u : 0u;
             fw[q] = ~0ull;
             if (g.filt && look[q] && ko[q].lb >= kFMin) {
-                fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift)];
+                fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift, g.fscale)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift, g.fscale)];
                 if constexpr (kCount) cn[kCntFilter]++;
             }
         }
@@ -468,7 +468,7 @@ struct PeelPolicy {
             for (int q = 0; q < U; q++) {
                 fw[q] = ~0ull;
                 if (look[q] && ko[q].lb >= kFMin) {
-                    fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift)];
+                    fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift, g.fscale)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift, g.fscale)];
                     if constexpr (kCount) cn[kCntFilter]++;
                 }
             }
@@ -1339,7 +1339,7 @@ __global__ void __launch_bounds__(256) k_rb_big(DevGraph g, PeelBufs pb) {
             const uint32_t b0 = pb.hbo_w[x], nb = pb.hbo_w[x + 1] - b0;
             TDG_CHECK(nb > 0 && uint64_t(b0) + nb <= g.nbuckets);
             if (nb > kHMid) bucket_insert(pb.htab_w + 8ull * b0, nb, y, static_cast<uint32_t>(e));
-            if (pb.filt_w && nb >= kFMin) atomicOr(&pb.filt_w[fword_index(b0, nb, y, kFShiftRebuild)], fbits(hmix(y)));
+            if (pb.filt_w && nb >= kFMin) atomicOr(&pb.filt_w[fword_index(b0, nb, y, kFShiftRebuild, g.fscale)], fbits(hmix(y)));
         }
     }
 }

@@ -195,7 +195,7 @@ constexpr uint32_t kHMid = 8 * kHSmall;  // block-built tables use the block's w
 #endif
 constexpr uint32_t kFMin = TDG_FMIN;
 #ifndef TDG_FSHIFT
-#define TDG_FSHIFT 3  // 4 bits per key: sparser filters stay L2-resident (C5: 16 -> 8 -> 4 bits, 3.47 -> 3.26 -> 3.19 s)
+#define TDG_FSHIFT 2  // 8 bits per key (with hashed word choice 4 bits won: sparser filters stayed L2-resident; with the rank-ordered choice (TDG_FMONO) lanes share sectors and the lower false-positive rate wins: C5 peel 2028 -> 1990 ms)
 #endif
 #ifndef TDG_FK
 #define TDG_FK 3  // bits set per key
@@ -224,9 +224,31 @@ __device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(k
 // Filter word of key y in the filter of a vertex whose table is buckets [ob, ob + nb).
 // (fshift: kFShift for the tables of the input graph; the peel's rebuilds on the live graph
 // use the denser kFShiftRebuild — a template parameter of the k_peel segments.)
-__device__ __forceinline__ uint64_t fword_index(uint32_t ob, uint32_t nb, uint32_t y, uint32_t fshift = kFShift) {
+// TDG_FMONO: the word is chosen by the key's RANK in the id space (y * fscale, fscale =
+// floor((2^32 - 1) / n): monotone in y) instead of by a hash, so the sorted list elements a warp
+// probes together fall into neighbouring words — lanes share filter sectors whenever the probe
+// list is not much shorter than the searched one. The bits inside the word stay hashed. With
+// clustered neighbour ids some words saturate (more false positives, never a wrong answer).
+#ifndef TDG_FMONO
+#define TDG_FMONO 1  // C5 peel 2101 -> 2028 ms
+#endif
+#ifndef TDG_FSCALE_END
+#define TDG_FSCALE_END 1  // fscale as the LAST DevGraph member: in front of the pointers it shifted the kernel
+                          // parameter layout and cost the probe loop 4 % (C5 peel 2101 -> 2186 ms)
+#endif
+// (TDG_FMONO = 2: a shift instead of the multiplier — exact when n is a power of two, else up
+// to half of a filter's words stay unused)
+__host__ __device__ __forceinline__ uint32_t filter_scale(uint32_t n) {
+    if (TDG_FMONO == 2) {
+        uint32_t sh = 0;
+        while (sh < 31 && (static_cast<unsigned long long>(n ? n - 1 : 0) << (sh + 1)) <= 0xffffffffull) sh++;
+        return sh;
+    }
+    return n ? 0xffffffffu / n : 0u;
+}
+__device__ __forceinline__ uint64_t fword_index(uint32_t ob, uint32_t nb, uint32_t y, uint32_t fshift, uint32_t fscale) {
     const uint32_t f0 = ob >> fshift, f1 = (ob + nb) >> fshift;
-    return static_cast<uint64_t>(f0) + __umulhi(fword(y), f1 - f0);
+    return static_cast<uint64_t>(f0) + __umulhi(TDG_FMONO == 2 ? y << fscale : TDG_FMONO ? y * fscale : fword(y), f1 - f0);
 }
 
 struct DevGraph {
@@ -235,6 +257,9 @@ struct DevGraph {
     const uint32_t* htab = nullptr;  // bucketed hash tables: 8 u32 words (4 keys, 4 values) per bucket
     const uint32_t* hbo = nullptr;   // n+1 bucket offsets
     const unsigned long long* filt = nullptr;  // membership filters of the big tables (or null)
+#if !TDG_FSCALE_END
+    uint32_t fscale = 0;             // filter_scale(n) (TDG_FMONO)
+#endif
     const uint32_t* off = nullptr;
     uint32_t* adj = nullptr;
     uint32_t* eid = nullptr;
@@ -247,6 +272,9 @@ struct DevGraph {
     const uint32_t* stask = nullptr;  // support tasks (slot index), see build.cu k_svalid
     const uint32_t* sx = nullptr;     // owner vertex of each support task's slot
     const uint32_t* sbeg = nullptr;   // n+1: first support task of each owner
+#if TDG_FSCALE_END
+    uint32_t fscale = 0;             // filter_scale(n) (TDG_FMONO)
+#endif
 };
 
 }  // namespace tdg
