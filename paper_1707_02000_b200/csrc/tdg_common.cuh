@@ -218,6 +218,7 @@ __device__ __forceinline__ uint32_t fword(uint32_t x) {
 __device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(key)
     unsigned long long b = (1ull << ((h >> 14) & 63)) | (1ull << ((h >> 20) & 63));
     if (TDG_FK > 2) b |= 1ull << ((h >> 26) & 63);
+    if (TDG_FK > 3) b |= 1ull << ((h >> 8) & 63);
     return b;
 }
 
