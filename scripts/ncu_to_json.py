@@ -11,7 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out")
-out = {"_doc": "ncu --replay-mode kernel, per launch (scripts/ncu_traffic.sh); dram_bytes = dram__bytes_read.sum + "
+out = {"_doc": "ncu --replay-mode kernel, per decomposition (k_peel: its segments summed; scripts/ncu_traffic.sh); dram_bytes = dram__bytes_read.sum + "
                "dram__bytes_write.sum; atom/red = lts__t_sectors_op_atom/red.sum",
        "src_sha": open(os.path.join(src, "ncu_src_sha.txt")).read().strip()}
 for f in sorted(glob.glob(os.path.join(src, "ncu_traffic_C*.csv"))):
@@ -46,15 +46,21 @@ for f in sorted(glob.glob(os.path.join(src, "ncu_traffic_C*.csv"))):
         k["ms"] = k.get("ms", 0) + d.get("gpu__time_duration.sum", 0)
         k["dram_bytes"] = k.get("dram_bytes", 0) + d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
         k["dram_read"] = k.get("dram_read", 0) + d.get("dram__bytes_read.sum", 0)
-        k["l2_hit_pct"] = d.get("lts__t_sector_hit_rate.pct")
+        k.setdefault("l2_hit_pct_by_launch", []).append(d.get("lts__t_sector_hit_rate.pct"))
+        k.setdefault("ms_by_launch", []).append(round(d.get("gpu__time_duration.sum", 0), 3))
         for m_ in ("lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum", "lts__t_requests_op_atom.sum",
                    "lts__t_requests_op_red.sum", "sm__inst_executed.sum"):
             k[m_] = k.get(m_, 0) + d.get(m_, 0)
-    for k in cf.values():  # per launch
-        L = max(k["launches"], 1)
+    # per DECOMPOSITION: k_peel is one logical launch cut into segments (table rebuilds in
+    # between); k_support_tab launches once per decomposition
+    D = max(cf.get("k_support_tab", {}).get("launches", 1), 1)
+    for k in cf.values():
         for m_ in list(k):
-            if m_ not in ("launches", "l2_hit_pct"):
-                k[m_] = k[m_] / L
+            if m_ not in ("launches", "l2_hit_pct_by_launch", "ms_by_launch"):
+                k[m_] = k[m_] / D
+        w = k["ms_by_launch"]
+        k["l2_hit_pct"] = round(sum(a * b for a, b in zip(k["l2_hit_pct_by_launch"], w)) / max(sum(w), 1e-9), 2)
+        k["launches_per_decomposition"] = k["launches"] / D
     out[f"C{cfg}"] = cf
 dst = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "ncu_traffic.json")
 json.dump(out, open(dst, "w"), indent=1)
