@@ -240,6 +240,13 @@ enum {
     TDG_NCOUNTERS
 };
 int tdg_counters(tdg_context* ctx, uint64_t* out, uint64_t cap);
+/* Diagnostic (no reference counterpart): how the membership filters of the graph resident
+ * in ctx (the last truss / step call) choose a key's word — *hashed = 0: by the key's rank in
+ * the id space (sorted probe lists share filter sectors), 1: by a multiplicative hash (chosen
+ * on the device when rank-mode filters would pass too many probes: clustered vertex ids);
+ * *fp_estimate = the probe-weighted false-positive estimate of the rank-mode fill. Results
+ * never depend on the mode. Synchronises the stream. */
+int tdg_filter_mode(tdg_context* ctx, int* hashed, double* fp_estimate);
 
 #ifdef __cplusplus
 }

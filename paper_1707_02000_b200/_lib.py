@@ -79,6 +79,7 @@ SIGNATURES = [
     ("tdg_truss", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp, _u64, _P(_u64), _P(tdg_times)]),
     ("tdg_truss_device", _i32, [_vp, _P(tdg_csr), _vp, _vp, _vp, _u64, _P(_u64), _P(tdg_times)]),
     ("tdg_counters", _i32, [_vp, _P(_u64), _u64]),
+    ("tdg_filter_mode", _i32, [_vp, _P(C.c_int), _P(C.c_double)]),
     ("tdg_support", _i32, [_vp, _P(tdg_csr), _vp, _P(tdg_times)]),
     ("tdg_support_device", _i32, [_vp, _P(tdg_csr), _vp, _P(tdg_times)]),
     ("tdg_support_shard", _i32, [_vp, _P(tdg_csr), _u32, _u32, _vp, _P(tdg_times)]),

@@ -205,10 +205,13 @@ __global__ void k_hinsert(const uint32_t* __restrict__ off, const uint32_t* __re
     }
 }
 
-// Filter bits of every slot (x -> y) whose owner table is big enough (tdg_common.cuh).
+// Filter bits of every slot (x -> y) whose owner table is big enough (tdg_common.cuh). `pass`
+// 0: the rank-mode fill; 1: the hash-mode refill, a no-op unless k_fdecide chose it.
 __global__ void k_finsert(const uint32_t* __restrict__ hbo, const uint32_t* __restrict__ adj,
                           const uint32_t* __restrict__ src, uint64_t slots, unsigned long long* __restrict__ filt,
-                          uint32_t fscale) {
+                          const FilterCtl* __restrict__ fc, int pass) {
+    if (pass == 1 && !fc->hashed) return;
+    const uint32_t fscale = fc->fscale;
     for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < slots;
          j += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t x = src[j];
@@ -217,6 +220,53 @@ __global__ void k_finsert(const uint32_t* __restrict__ hbo, const uint32_t* __re
         const uint32_t y = adj[j];
         atomicOr(&filt[fword_index(b0, nb, y, kFShift, fscale)], fbits(hmix(y)));
     }
+}
+
+__global__ void k_fctl_init(FilterCtl* fc, uint32_t n) {
+    fc->fscale = TDG_FMONO ? filter_scale(n) : kFilterHashMul;
+    fc->hashed = TDG_FMONO ? 0u : 1u;
+    fc->keys = 0;
+    fc->fp = 0;
+}
+
+// Probe-weighted false-positive estimate of the rank-mode filters: a word with p bits set
+// passes a 3-bit probe with probability ~ (p/64)^3, and receives probes in proportion to the
+// keys it holds (the probe lists are neighbour lists of the same id space), ~ p. Sums of p and
+// of p * (p/64)^3 (in 2^-18 units) over all words.
+__global__ void k_fstat(const unsigned long long* __restrict__ filt, uint64_t words, FilterCtl* fc) {
+    unsigned long long keys = 0, fp = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words; i += uint64_t(gridDim.x) * blockDim.x) {
+        const unsigned long long p = static_cast<unsigned long long>(__popcll(filt[i]));
+        keys += p;
+        fp += p * p * p * p;  // p * (p/64)^3 * 2^18
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        keys += __shfl_xor_sync(0xffffffffu, keys, o);
+        fp += __shfl_xor_sync(0xffffffffu, fp, o);
+    }
+    if ((threadIdx.x & 31) == 0 && keys) {
+        atomicAdd(&fc->keys, keys);
+        atomicAdd(&fc->fp, fp);
+    }
+}
+
+// Hash mode when the estimate exceeds kFilterFpMax (balanced 8-bit-per-key words sit near 0.05;
+// a hashed fill of any graph stays there).
+#ifndef TDG_FILTER_FP_MAX
+#define TDG_FILTER_FP_MAX 0.12
+#endif
+__global__ void k_fdecide(FilterCtl* fc) {
+    const double est = fc->keys ? static_cast<double>(fc->fp) / 262144.0 / static_cast<double>(fc->keys) : 0.0;
+    if (TDG_FMONO && est > TDG_FILTER_FP_MAX) {
+        fc->hashed = 1;
+        fc->fscale = kFilterHashMul;
+    }
+}
+
+__global__ void k_fclear_if_hashed(unsigned long long* __restrict__ filt, uint64_t words, const FilterCtl* __restrict__ fc) {
+    if (!fc->hashed) return;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words; i += uint64_t(gridDim.x) * blockDim.x)
+        filt[i] = 0ull;
 }
 
 // Support-pass task list: each oriented edge a->b is owned by the endpoint whose N+ list
@@ -420,14 +470,25 @@ cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uin
 }
 
 cudaError_t launch_filter_fill(const uint32_t* hbo, const uint32_t* adj, const uint32_t* src, uint32_t n, uint32_t m,
-                               unsigned long long* filt, cudaStream_t st, uint32_t* launches) {
-    if (m == 0) return cudaSuccess;
-    cudaError_t err = cudaMemsetAsync(filt, 0, filter_words(n, m) * sizeof(unsigned long long), st);
+                               unsigned long long* filt, FilterCtl* fctl, cudaStream_t st, uint32_t* launches) {
+    k_fctl_init<<<1, 1, 0, st>>>(fctl, n);
+    (*launches)++;
+    if (m == 0) return cudaGetLastError();
+    const uint64_t words = filter_words(n, m);
+    cudaError_t err = cudaMemsetAsync(filt, 0, words * sizeof(unsigned long long), st);
     if (err != cudaSuccess) return err;
     const uint64_t slots = 2ull * m;
     const unsigned gs = grid_for(slots) > 148u * 64u ? 148u * 64u : grid_for(slots);
-    k_finsert<<<gs, kThreads, 0, st>>>(hbo, adj, src, slots, filt, filter_scale(n));
+    k_finsert<<<gs, kThreads, 0, st>>>(hbo, adj, src, slots, filt, fctl, 0);
     (*launches)++;
+    if (TDG_FMONO) {  // rank mode unless the filters it produced pass too much (tdg_common.cuh)
+        const unsigned gw = grid_for(words) > 148u * 16u ? 148u * 16u : grid_for(words);
+        k_fstat<<<gw, kThreads, 0, st>>>(filt, words, fctl);
+        k_fdecide<<<1, 1, 0, st>>>(fctl);
+        k_fclear_if_hashed<<<gw, kThreads, 0, st>>>(filt, words, fctl);
+        k_finsert<<<gs, kThreads, 0, st>>>(hbo, adj, src, slots, filt, fctl, 1);
+        (*launches) += 4;
+    }
     return cudaGetLastError();
 }
 

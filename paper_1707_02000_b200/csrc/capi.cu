@@ -93,6 +93,7 @@ struct tdg_context {
     // one arena for the m-sized scratch: the build + support arrays and the peel lists share
     // it (they are never live at the same time; layout in ensure_arena)
     DevBuf arena;
+    DevBuf fctl;  // FilterCtl of the resident graph
     DevBuf cchunk, nsl, ctl, sctl, sacc, cub, truss, sup, f0, f1, f2, bsum, bhist, bcur, trace;
     DevBuf kdeg, kcore, kL0, kL1, kA0, kA1, kwpre, kctl, ktmp, knoff, knadj, kperm, kbad, ing, ptext, pscr, ppairs;
     // arena views (recomputed by ensure_arena)
@@ -212,7 +213,7 @@ struct tdg_context {
         g.hbo = hbo.as<uint32_t>();
         g.nbuckets = htab.cap / 32;
         g.filt = peel_filter() ? filt.as<unsigned long long>() : nullptr;
-        g.fscale = filter_scale(n);
+        g.fctl = fctl.as<FilterCtl>();
         return g;
     }
     PeelBufs peel_bufs(uint32_t n) const {
@@ -270,7 +271,7 @@ struct tdg_context {
         return p;
     }
     void trim() {
-        DevBuf* all[] = {&off64, &off, &adj, &eo, &up, &P, &eid, &el, &opos, &oeid, &sbeg, &dl, &pbits, &hbo, &htab, &filt,
+        DevBuf* all[] = {&fctl, &off64, &off, &adj, &eo, &up, &P, &eid, &el, &opos, &oeid, &sbeg, &dl, &pbits, &hbo, &htab, &filt,
                          &arena, &cchunk, &nsl, &ctl, &sctl, &sacc, &cub, &truss, &sup, &f0, &f1, &f2, &bsum, &bhist,
                          &bcur, &trace, &kdeg, &kcore, &kL0, &kL1, &kA0, &kA1, &kwpre, &kctl, &ktmp, &knoff, &knadj,
                          &kperm, &kbad, &ing, &ptext, &pscr, &ppairs};
@@ -446,8 +447,10 @@ void stage_and_build(tdg_context* c, const tdg_csr* g, Dims d, bool host_ptrs, b
                             c->stream, &c->launches), "hash fill");
         if (peel_filter()) {
             c->filt.ensure(filter_words(d.n, d.m) * 8, "filters");
+            c->fctl.ensure(sizeof(FilterCtl), "filter control");
             ck(launch_filter_fill(c->hbo.as<uint32_t>(), c->adj.as<uint32_t>(), c->src, d.n, d.m,
-                                  c->filt.as<unsigned long long>(), c->stream, &c->launches), "filter fill");
+                                  c->filt.as<unsigned long long>(), c->fctl.as<FilterCtl>(), c->stream, &c->launches),
+               "filter fill");
         }
     }
     ck(cudaEventRecord(c->ev[2], c->stream), "event");
@@ -526,6 +529,12 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
                                  h[4 * i + 2], h[4 * i + 3]);
                 std::fclose(f);
             }
+        }
+        if (std::getenv("TDG_FILTER_DEBUG") && c->fctl.p && peel_filter() && d.m) {  // diagnostic: filter mode of this graph
+            FilterCtl fc;
+            d2h(c->stream, &fc, c->fctl.p, sizeof(fc), "D2H filter control");
+            std::fprintf(stderr, "tdg filter: %s mode, fp estimate %.4f (keys %llu)\n", fc.hashed ? "hash" : "rank",
+                         fc.keys ? double(fc.fp) / 262144.0 / double(fc.keys) : 0.0, fc.keys);
         }
         if (nsl_len) *nsl_len = len;
         if (nsl_out && len) {
@@ -1059,6 +1068,18 @@ int tdg_counters(tdg_context* ctx, uint64_t* out, uint64_t cap) {
         v[TDG_CNT_SUP_SEARCH] = c->hctl->sup.search_items;
         v[TDG_CNT_SUP_HUB] = c->hctl->sup.hub_items;
         for (uint64_t i = 0; i < cap && i < TDG_NCOUNTERS; i++) out[i] = v[i];
+    });
+}
+
+int tdg_filter_mode(tdg_context* ctx, int* hashed, double* fp_estimate) {
+    return guarded([&] {
+        tdg_context* c = resolve(ctx);
+        c->use();
+        if (!c->fctl.p) throw Fail{TDG_ERR_INVALID, "no filtered graph is resident in this context"};
+        FilterCtl fc;
+        d2h(c->stream, &fc, c->fctl.p, sizeof(fc), "D2H filter control");
+        if (hashed) *hashed = fc.hashed ? 1 : 0;
+        if (fp_estimate) *fp_estimate = fc.keys ? double(fc.fp) / 262144.0 / double(fc.keys) : 0.0;
     });
 }
 

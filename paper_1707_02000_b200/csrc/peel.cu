@@ -386,6 +386,7 @@ struct PeelPolicy {
         bool look[U];
         uint32_t pw[U];
         unsigned long long fw[U];
+        const uint32_t fscale = g.filt ? __ldg(&g.fctl->fscale) : 0u;  // (uniform; FilterCtl, tdg_common.cuh)
 #pragma unroll
         for (int q = 0; q < U; q++) {
             look[q] = act[q];
@@ -394,7 +395,7 @@ struct PeelPolicy {
             if constexpr (kCount) cn[kCntPbits] += (pbits && look[q]) ? 1u : 0u;
             fw[q] = ~0ull;
             if (g.filt && look[q] && ko[q].lb >= kFMin) {
-                fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift, g.fscale)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift, g.fscale)];
+                fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift, fscale)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift, fscale)];
                 if constexpr (kCount) cn[kCntFilter]++;
             }
         }
@@ -464,11 +465,12 @@ struct PeelPolicy {
         }
         if (g.filt) {
             unsigned long long fw[U];
+            const uint32_t fscale = __ldg(&g.fctl->fscale);
 #pragma unroll
             for (int q = 0; q < U; q++) {
                 fw[q] = ~0ull;
                 if (look[q] && ko[q].lb >= kFMin) {
-                    fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift, g.fscale)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift, g.fscale)];
+                    fw[q] = TDG_FILT_NC ? __ldg(g.filt + fword_index(ko[q].ob, ko[q].lb, x[q], kShift, fscale)) : g.filt[fword_index(ko[q].ob, ko[q].lb, x[q], kShift, fscale)];
                     if constexpr (kCount) cn[kCntFilter]++;
                 }
             }
@@ -1328,6 +1330,7 @@ __global__ void __launch_bounds__(256) k_rb_small(DevGraph g, PeelBufs pb) {
 __global__ void __launch_bounds__(256) k_rb_big(DevGraph g, PeelBufs pb) {
     if (pb.ctl->done) return;
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint32_t fscale = pb.filt_w ? g.fctl->fscale : 0u;
     for (uint64_t e0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; e0 < g.m; e0 += stride) {
         const uint32_t w = pb.pbits[e0 >> 5];
         const uint64_t e = e0 + lane_id();
@@ -1339,7 +1342,7 @@ __global__ void __launch_bounds__(256) k_rb_big(DevGraph g, PeelBufs pb) {
             const uint32_t b0 = pb.hbo_w[x], nb = pb.hbo_w[x + 1] - b0;
             TDG_CHECK(nb > 0 && uint64_t(b0) + nb <= g.nbuckets);
             if (nb > kHMid) bucket_insert(pb.htab_w + 8ull * b0, nb, y, static_cast<uint32_t>(e));
-            if (pb.filt_w && nb >= kFMin) atomicOr(&pb.filt_w[fword_index(b0, nb, y, kFShiftRebuild, g.fscale)], fbits(hmix(y)));
+            if (pb.filt_w && nb >= kFMin) atomicOr(&pb.filt_w[fword_index(b0, nb, y, kFShiftRebuild, fscale)], fbits(hmix(y)));
         }
     }
 }

@@ -208,13 +208,6 @@ constexpr uint32_t kFShiftRebuild = TDG_FSHIFT_REBUILD;
 static_assert(kFShiftRebuild <= kFShift, "rebuilt filters may be denser, never sparser (TDG_FMIN covers both)");
 static_assert((kFMin >> kFShift) >= 1, "every filtered vertex owns at least one filter word");
 
-__device__ __forceinline__ uint32_t fword(uint32_t x) {
-    x = (x ^ 0x9e3779b9u) * 0x85ebca6bu;
-    x ^= x >> 15;
-    x *= 0xc2b2ae35u;
-    x ^= x >> 13;
-    return x;
-}
 __device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(key)
     unsigned long long b = (1ull << ((h >> 14) & 63)) | (1ull << ((h >> 20) & 63));
     if (TDG_FK > 2) b |= 1ull << ((h >> 26) & 63);
@@ -225,31 +218,31 @@ __device__ __forceinline__ unsigned long long fbits(uint32_t h) {  // h = hmix(k
 // Filter word of key y in the filter of a vertex whose table is buckets [ob, ob + nb).
 // (fshift: kFShift for the tables of the input graph; the peel's rebuilds on the live graph
 // use the denser kFShiftRebuild — a template parameter of the k_peel segments.)
-// TDG_FMONO: the word is chosen by the key's RANK in the id space (y * fscale, fscale =
-// floor((2^32 - 1) / n): monotone in y) instead of by a hash, so the sorted list elements a warp
-// probes together fall into neighbouring words — lanes share filter sectors whenever the probe
-// list is not much shorter than the searched one. The bits inside the word stay hashed. With
-// clustered neighbour ids some words saturate (more false positives, never a wrong answer).
+// The word of a key is umulhi(y * fscale, words of the vertex). Two multipliers (FilterCtl,
+// chosen per graph by build.cu, read by the kernels from device memory — no host round trip):
+//  * RANK mode, fscale = floor((2^32 - 1) / n): monotone in y, so the sorted list elements a
+//    warp probes together fall into neighbouring words and share filter sectors (about
+//    d(b)/d(a) sectors per warp step instead of 32). Right when neighbour ids are spread over
+//    the id space (permuted / hashed ids): C5 peel 2101 -> 1990 ms.
+//  * HASH mode, fscale = 0x9E3779B1 (multiplicative hashing): when ids are clustered (an
+//    unpermuted RMAT: hubs and their neighbours sit at low ids) rank mode piles the keys of a
+//    vertex into few words, which saturate and pass every probe (measured: peel +21..32 %).
+// After a rank-mode fill the build measures the probe-weighted false-positive estimate of the
+// filters and refills them in hash mode when it is too high (kFilterFpMax). The bits inside
+// the word are hashed in both modes. TDG_FMONO = 0 compiles the rank mode out.
 #ifndef TDG_FMONO
-#define TDG_FMONO 1  // C5 peel 2101 -> 2028 ms
+#define TDG_FMONO 1
 #endif
-#ifndef TDG_FSCALE_END
-#define TDG_FSCALE_END 1  // fscale as the LAST DevGraph member: in front of the pointers it shifted the kernel
-                          // parameter layout and cost the probe loop 4 % (C5 peel 2101 -> 2186 ms)
-#endif
-// (TDG_FMONO = 2: a shift instead of the multiplier — exact when n is a power of two, else up
-// to half of a filter's words stay unused)
-__host__ __device__ __forceinline__ uint32_t filter_scale(uint32_t n) {
-    if (TDG_FMONO == 2) {
-        uint32_t sh = 0;
-        while (sh < 31 && (static_cast<unsigned long long>(n ? n - 1 : 0) << (sh + 1)) <= 0xffffffffull) sh++;
-        return sh;
-    }
-    return n ? 0xffffffffu / n : 0u;
-}
+constexpr uint32_t kFilterHashMul = 0x9E3779B1u;
+__host__ __device__ __forceinline__ uint32_t filter_scale(uint32_t n) { return n ? 0xffffffffu / n : 0u; }
+struct FilterCtl {
+    uint32_t fscale;   // the multiplier in use
+    uint32_t hashed;   // 1: hash mode was chosen (filters refilled)
+    unsigned long long keys, fp;  // sum over words of set bits, and of set bits x (fill^3) in 2^-18 units
+};
 __device__ __forceinline__ uint64_t fword_index(uint32_t ob, uint32_t nb, uint32_t y, uint32_t fshift, uint32_t fscale) {
     const uint32_t f0 = ob >> fshift, f1 = (ob + nb) >> fshift;
-    return static_cast<uint64_t>(f0) + __umulhi(TDG_FMONO == 2 ? y << fscale : TDG_FMONO ? y * fscale : fword(y), f1 - f0);
+    return static_cast<uint64_t>(f0) + __umulhi(y * fscale, f1 - f0);
 }
 
 struct DevGraph {
@@ -258,9 +251,6 @@ struct DevGraph {
     const uint32_t* htab = nullptr;  // bucketed hash tables: 8 u32 words (4 keys, 4 values) per bucket
     const uint32_t* hbo = nullptr;   // n+1 bucket offsets
     const unsigned long long* filt = nullptr;  // membership filters of the big tables (or null)
-#if !TDG_FSCALE_END
-    uint32_t fscale = 0;             // filter_scale(n) (TDG_FMONO)
-#endif
     const uint32_t* off = nullptr;
     uint32_t* adj = nullptr;
     uint32_t* eid = nullptr;
@@ -273,9 +263,9 @@ struct DevGraph {
     const uint32_t* stask = nullptr;  // support tasks (slot index), see build.cu k_svalid
     const uint32_t* sx = nullptr;     // owner vertex of each support task's slot
     const uint32_t* sbeg = nullptr;   // n+1: first support task of each owner
-#if TDG_FSCALE_END
-    uint32_t fscale = 0;             // filter_scale(n) (TDG_FMONO)
-#endif
+    // (kept LAST: a member in front of the pointers shifted the kernel parameter layout and cost
+    // the peel's probe loop 4 %, C5 2101 -> 2186 ms)
+    const FilterCtl* fctl = nullptr;  // filter word multiplier of this graph (device memory)
 };
 
 }  // namespace tdg

@@ -52,8 +52,10 @@ inline uint64_t filter_words(uint64_t n, uint64_t m) { return (htab_buckets(n, m
 cudaError_t launch_htab_fill(const uint32_t* off, const uint32_t* adj, const uint32_t* src, const uint32_t* eid,
                              uint32_t n, uint32_t m, uint32_t* hq, uint32_t* hbo, uint32_t* htab, void* cub_tmp,
                              size_t cub_bytes, cudaStream_t st, uint32_t* launches);
+// fctl: the graph's FilterCtl (word multiplier: rank mode, or hash mode when rank-mode filters
+// would pass too much; decided on the device).
 cudaError_t launch_filter_fill(const uint32_t* hbo, const uint32_t* adj, const uint32_t* src, uint32_t n, uint32_t m,
-                               unsigned long long* filt, cudaStream_t st, uint32_t* launches);
+                               unsigned long long* filt, FilterCtl* fctl, cudaStream_t st, uint32_t* launches);
 
 struct StatsAcc {
     unsigned long long d_max, sum_deg_sq, sum_dplus_sq, deg_sum_dplus_sq, deg_s1;

@@ -223,6 +223,13 @@ class Context:
         return dict(zip(self.COUNTER_NAMES, list(out)))
 
     # -- host-pointer entry points
+    def filter_mode(self) -> tuple[bool, float]:
+        """tdg_filter_mode: (hash mode chosen?, false-positive estimate of the rank-mode filters)
+        of the graph this context last decomposed."""
+        h, e = C.c_int(), C.c_double()
+        _ck(_lib.tdg().tdg_filter_mode(self._h, C.byref(h), C.byref(e)))
+        return bool(h.value), e.value
+
     def truss(self, g: CsrGraph, want_support: bool = False):
         """tdg_truss: returns (truss u32[m], nsl list, support or None, times dict)."""
         truss = np.zeros(max(g.m, 1), np.uint32)
