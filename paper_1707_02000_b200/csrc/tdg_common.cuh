@@ -83,36 +83,6 @@ __device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t* __restrict__
     return static_cast<uint32_t>(base - a) + (*base <= x);
 }
 
-// Warp-cooperative search (all 32 lanes call with the same arguments): first index in
-// [0,len) with a[i] > x (kUpper) or a[i] >= x, len if none. 32-ary: each round samples 32
-// positions with one load per lane, so a list of L entries costs ~log32(L) dependent
-// round trips instead of the log2(L) of a single-lane binary search.
-template <bool kUpper>
-__device__ __forceinline__ uint32_t warp_bound_u32(const uint32_t* __restrict__ a, uint32_t len, uint32_t x) {
-    const uint32_t lane = lane_id();
-    uint32_t lo = 0, hi = len;  // answer in [lo, hi]
-    while (hi - lo > 32) {
-        const uint32_t step = (hi - lo + 31) / 32;
-        const uint32_t idx = lo + lane * step;
-        bool below = false;
-        if (idx < hi) {
-            const uint32_t v = a[idx];
-            below = kUpper ? v <= x : v < x;
-        }
-        const uint32_t cnt = __popc(__ballot_sync(kFull, below));
-        const uint32_t nlo = cnt ? lo + (cnt - 1) * step + 1 : lo;
-        const uint32_t nhi = min(hi, lo + cnt * step);
-        lo = nlo;
-        hi = nhi;
-    }
-    bool below = false;
-    if (lo + lane < hi) {
-        const uint32_t v = a[lo + lane];
-        below = kUpper ? v <= x : v < x;
-    }
-    return lo + __popc(__ballot_sync(kFull, below));
-}
-
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
