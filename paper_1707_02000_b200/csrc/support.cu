@@ -142,7 +142,11 @@ static_assert(kSupTab % 4 == 0 && kSupCap < 65536, "bucketed owner table: u16 po
 #ifndef TDG_SUP_MINB
 #define TDG_SUP_MINB 4  // 64 registers: the 8-probe-per-lane quad step needs them (C5: MINB 5 797 ms, 4 774 ms, 3 878 ms)
 #endif
-constexpr uint32_t kSupWarps = kThreads / 32;
+#ifndef TDG_SUP_THREADS
+#define TDG_SUP_THREADS 256  // threads of a k_support_tab block (the unit that shares one owner table)
+#endif
+constexpr int kTabThreads = TDG_SUP_THREADS;
+constexpr uint32_t kSupWarps = kTabThreads / 32;
 
 // Shared-memory table slot of key c: multiplicative (Fibonacci) hashing, top bits of
 // c * 2^32/phi — one multiply and a shift instead of hmix's five-step mix (the support pass
@@ -243,14 +247,14 @@ __device__ __forceinline__ uint32_t task_in(unsigned long long x, uint32_t lo, u
     return lo;
 }
 
-__global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
+__global__ void __launch_bounds__(kTabThreads, TDG_SUP_MINB) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
                                                           const unsigned long long* wpre, const unsigned long long* bsum,
                                                           uint32_t nchunks, SupportCtl* ctl, uint32_t shard,
                                                           uint32_t nshards) {
     extern __shared__ uint4 tab_keys4[];  // kSupTab keys, then kSupTab u16 positions, then kSupTab u16 counters
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     __shared__ uint32_t sh_p;
-    const unsigned long long W = chunk_offsets<kThreads>(bsum, nchunks, sboff);
+    const unsigned long long W = chunk_offsets<kTabThreads>(bsum, nchunks, sboff);
     if (W == 0) return;
     // Shard `shard` of `nshards` (the support pass shards with no exchange but a
     // final sum) owns the contiguous stretch [Wlo, Whi) of the work axis: equal probe work per
@@ -317,11 +321,11 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
                 uint32_t size = 64;
                 while (size < TDG_SUP_LOAD * nk && size < kSupTab) size <<= 1;  // load <= 1/LOAD, or <= 3/4 at full size
                 const uint32_t bmask = size / 4 - 1;
-                for (uint32_t q = threadIdx.x; q < size / 4; q += kThreads)
+                for (uint32_t q = threadIdx.x; q < size / 4; q += kTabThreads)
                     tab_keys4[q] = make_uint4(kHEmpty, kHEmpty, kHEmpty, kHEmpty);
-                for (uint32_t q = threadIdx.x; q < size / 2; q += kThreads) cnt2[q] = 0;
+                for (uint32_t q = threadIdx.x; q < size / 2; q += kTabThreads) cnt2[q] = 0;
                 __syncthreads();
-                for (uint32_t q = threadIdx.x; q < nk; q += kThreads) {
+                for (uint32_t q = threadIdx.x; q < nk; q += kTabThreads) {
                     const uint32_t c = g.oadj[o + p0 + q];
                     uint32_t b = tab_hash(c, bmask);
                     while (true) {  // first free slot of the bucket (slots fill in order), else the next bucket
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, TDG_SUP_MINB) k_support_tab(DevGraph
                 }
                 __syncthreads();
                 // flush the slots' hit counters: s[slot of x -> key] += count
-                for (uint32_t q = threadIdx.x; q < size / 2; q += kThreads) {
+                for (uint32_t q = threadIdx.x; q < size / 2; q += kTabThreads) {
                     const uint32_t c2 = cnt2[q];
                     if (c2 & 0xffffu) atomicAdd(&s[o + p0 + tpos[2u * q]], c2 & 0xffffu);
                     if (c2 >> 16) atomicAdd(&s[o + p0 + tpos[2u * q + 1]], c2 >> 16);
@@ -455,9 +459,9 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* w
         err = cudaFuncSetAttribute(k_support_tab, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (err != cudaSuccess) return err;
         int tb = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb, k_support_tab, kThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb, k_support_tab, kTabThreads, smem);
         if (tb < 1) tb = 1;
-        k_support_tab<<<static_cast<unsigned>(sm_count * tb), kThreads, smem, st>>>(g, s, wpre, bsum, nchunks, ctl, shard,
+        k_support_tab<<<static_cast<unsigned>(sm_count * tb), kTabThreads, smem, st>>>(g, s, wpre, bsum, nchunks, ctl, shard,
                                                                                     nshards);
     } else {
         if (nshards != 1) return cudaErrorNotSupported;  // the diagnostic search form is unsharded
