@@ -81,6 +81,34 @@ def main():
     rows.append({"row": "canonicalize (graph.cpp:19-71), shuffled+flipped edge stream", "gpu_s": tg, "ref_s": tr,
                  "equal": eq})
 
+    # sharded support pass: R shards one after another on this GPU; the shards'
+    # partial supports must sum to the reference's support_am4, and the slowest shard shows the
+    # work balance (ideal = full / R)
+    t_full, s_full = timed(lambda: ctx.support(g)[0], 2)
+    tr, s_ref = timed(lambda: R.support_am4(c, threads))
+    for shards in (2, 8):
+        ts, acc = [], np.zeros(m, np.uint64)
+        for r_ in range(shards):
+            t_, part = timed(lambda: ctx.support_shard(g, r_, shards)[1]["support_ms"], 1)
+            ts.append(part)
+            acc += ctx.support_shard(g, r_, shards)[0]
+        rows.append({"row": f"support_am4 sharded x{shards} (triangle.cpp:26-61; kernel ms of the slowest shard)",
+                     "gpu_s": max(ts) * 1e-3, "ref_s": tr, "equal": bool((acc.astype(np.uint32) == s_ref).all()),
+                     "shard_ms": [round(x, 2) for x in ts], "full_kernel_ms": round(ctx.support(g)[1]["support_ms"], 2)})
+
+    # read_edge_list on a text file of the first 4M edges (graph.cpp:152-200)
+    import tempfile
+    k4 = min(len(pairs), 4_000_000)
+    with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
+        f.write("# bench_next\n")
+        np.savetxt(f, pairs[:k4], fmt="%d")
+        path = f.name
+    tg, pg = timed(lambda: trussdec.read_edge_list(path), 2)
+    tr, pr = timed(lambda: R.read_edge_list(path))
+    os.unlink(path)
+    rows.append({"row": f"read_edge_list, {k4} text lines (graph.cpp:152-200)", "gpu_s": tg, "ref_s": tr,
+                 "equal": bool(np.array_equal(np.asarray(pg, np.uint64).reshape(-1, 2), np.asarray(pr, np.uint64).reshape(-1, 2)))})
+
     for r in rows:
         r.update({"config": graphgen.CONFIG_NAMES[cfg], "m": m, "ref_threads": threads,
                   "speedup": (r["ref_s"] / r["gpu_s"]) if r.get("ref_s") else None})
