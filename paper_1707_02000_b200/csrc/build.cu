@@ -250,10 +250,13 @@ __global__ void k_fstat(const unsigned long long* __restrict__ filt, uint64_t wo
     }
 }
 
-// Hash mode when the estimate exceeds kFilterFpMax (balanced 8-bit-per-key words sit near 0.05;
-// a hashed fill of any graph stays there).
+// Hash mode when the estimate exceeds TDG_FILTER_FP_MAX. Balanced 8-bit-per-key words sit at
+// 0.046-0.047 (C3, C4, C5; a hashed fill of any graph stays there) and rank order then wins
+// 3.5 % of the peel; an unpermuted RMAT sits at 0.24 and rank order loses 21-32 %. Between the
+// two points the break-even is near 0.07; every extra point of false positives is one more
+// table sector per hundred probes.
 #ifndef TDG_FILTER_FP_MAX
-#define TDG_FILTER_FP_MAX 0.12
+#define TDG_FILTER_FP_MAX 0.08
 #endif
 __global__ void k_fdecide(FilterCtl* fc) {
     const double est = fc->keys ? static_cast<double>(fc->fp) / 262144.0 / static_cast<double>(fc->keys) : 0.0;
