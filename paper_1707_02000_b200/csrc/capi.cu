@@ -21,6 +21,11 @@
 using namespace tdg;
 namespace tdg { extern const char* g_ingest_step; }
 
+#ifndef TDG_SUP_TAB
+#define TDG_SUP_TAB_DEFAULT 4096
+#else
+#define TDG_SUP_TAB_DEFAULT TDG_SUP_TAB
+#endif
 namespace {
 
 thread_local std::string g_err;
@@ -530,6 +535,11 @@ int truss_impl(tdg_context* ctx, const tdg_csr* g, uint32_t* truss_out, uint32_t
                 std::fclose(f);
             }
         }
+        if (std::getenv("TDG_SUP_DEBUG"))  // diagnostic: block geometry of the support pass
+            std::fprintf(stderr, "tdg support: %s geometry, %.1f %% of the work has an owner list above %u keys\n",
+                         c->hctl->sup.big_geometry ? "big" : "small",
+                         c->hctl->sup.work_items ? 100.0 * double(c->hctl->sup.big_work) / double(c->hctl->sup.work_items) : 0.0,
+                         unsigned(TDG_SUP_TAB_DEFAULT / 4));
         if (std::getenv("TDG_FILTER_DEBUG") && c->fctl.p && peel_filter() && d.m) {  // diagnostic: filter mode of this graph
             FilterCtl fc;
             d2h(c->stream, &fc, c->fctl.p, sizeof(fc), "D2H filter control");

@@ -123,16 +123,26 @@ struct SupportPolicy {
 // loads. Hub owners whose list exceeds the table (d+ > kSupCap) run several passes, one per
 // kSupCap-key slice of the sorted N+(x); a pass skips the elements outside its key range.
 // Segments too small to pay for the table are batched and searched in global memory.
+// Two block geometries, chosen per graph on the device (k_support_prep measures the share of
+// the probe work whose owner list is longer than kSupBigDeg; every block of both launches reads
+// the same verdict and the other launch exits at once):
+//  * 256 threads x 4096-slot table, 4 blocks/SM: best when owner lists are short (C3, C4);
+//  * 512 threads x 8192-slot table, 2 blocks/SM (same warps per SM): owners of 1024 < d+ <= 2048
+//    keep the table at load <= 1/4 (fewer bucket walks) and d+ up to 6144 needs no slicing —
+//    C5 support 731 -> 680 ms, but C3 55 -> 61 ms (its segments are too small to fill 16 warps).
 #ifndef TDG_SUP_TAB
-#define TDG_SUP_TAB 4096  // shared-memory table slots (4 B key + 2 B position + 2 B counter)
+#define TDG_SUP_TAB 4096  // shared-memory table slots (4 B key + 2 B position + 2 B counter) of the small geometry
 #endif
 constexpr uint32_t kSupTab = TDG_SUP_TAB;
-constexpr uint32_t kSupCap = 3 * kSupTab / 4;  // keys per table at the full-size load of 3/4
+constexpr uint32_t kSupBigDeg = kSupTab / 4;  // owner lists longer than this load a small-geometry table above 1/4
+#ifndef TDG_SUP_BIG_PCT
+#define TDG_SUP_BIG_PCT 50  // big geometry when more than this share (%) of the probe work has such an owner (101: never)
+#endif
 #ifndef TDG_SUP_LOAD
 #define TDG_SUP_LOAD 4  // table slots per key when the table is not full size (C5: 2 -> 4: 1089 -> 1047 ms)
 #endif
-constexpr size_t kSupSmem = size_t(kSupTab) * (sizeof(uint32_t) + 2 * sizeof(uint16_t));
-static_assert(kSupTab % 4 == 0 && kSupCap < 65536, "bucketed owner table: u16 positions and counters");
+constexpr size_t sup_smem(uint32_t tab) { return size_t(tab) * (sizeof(uint32_t) + 2 * sizeof(uint16_t)); }
+static_assert(kSupTab % 4 == 0 && 3 * (2 * kSupTab) / 4 < 65536, "bucketed owner table: u16 positions and counters");
 #ifndef TDG_SUP_SEGMIN
 #define TDG_SUP_SEGMIN 512u  // a segment gets a table if its probes * SEGDIV >= max(d+(x), SEGMIN)
 #endif
@@ -146,7 +156,6 @@ static_assert(kSupTab % 4 == 0 && kSupCap < 65536, "bucketed owner table: u16 po
 #define TDG_SUP_THREADS 256  // threads of a k_support_tab block (the unit that shares one owner table)
 #endif
 constexpr int kTabThreads = TDG_SUP_THREADS;
-constexpr uint32_t kSupWarps = kTabThreads / 32;
 
 // Shared-memory table slot of key c: multiplicative (Fibonacci) hashing, top bits of
 // c * 2^32/phi — one multiply and a shift instead of hmix's five-step mix (the support pass
@@ -247,15 +256,27 @@ __device__ __forceinline__ uint32_t task_in(unsigned long long x, uint32_t lo, u
     return lo;
 }
 
-__global__ void __launch_bounds__(kTabThreads, TDG_SUP_MINB) k_support_tab(DevGraph g, uint32_t* __restrict__ s,
-                                                          const unsigned long long* wpre, const unsigned long long* bsum,
-                                                          uint32_t nchunks, SupportCtl* ctl, uint32_t shard,
-                                                          uint32_t nshards) {
+// kBig: 0 = the small geometry, 1 = the big one (twice the threads and table slots, half the blocks).
+template <int kBig>
+__global__ void __launch_bounds__(kTabThreads << kBig, TDG_SUP_MINB >> kBig) k_support_tab(
+    DevGraph g, uint32_t* __restrict__ s, const unsigned long long* wpre, const unsigned long long* bsum,
+    uint32_t nchunks, SupportCtl* ctl, uint32_t shard, uint32_t nshards, int force) {
+    constexpr int kTabThreads = tdg::kTabThreads << kBig;
+    constexpr uint32_t kSupTab = tdg::kSupTab << kBig;
+    constexpr uint32_t kSupCap = 3 * kSupTab / 4;  // keys per table at the full-size load of 3/4
+    constexpr uint32_t kSupWarps = kTabThreads / 32;
     extern __shared__ uint4 tab_keys4[];  // kSupTab keys, then kSupTab u16 positions, then kSupTab u16 counters
     __shared__ unsigned long long sboff[kMaxChunks + 1];
     __shared__ uint32_t sh_p;
     const unsigned long long W = chunk_offsets<kTabThreads>(bsum, nchunks, sboff);
     if (W == 0) return;
+    // the geometry of this graph (k_support_prep's tally; force: diagnostic override)
+    const bool big = force >= 0 ? force != 0 : ctl->big_work * 100ull > W * static_cast<unsigned long long>(TDG_SUP_BIG_PCT);
+    if (big != (kBig == 1)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->work_items = W;
+        ctl->big_geometry = kBig;
+    }
     // Shard `shard` of `nshards` (the support pass shards with no exchange but a
     // final sum) owns the contiguous stretch [Wlo, Whi) of the work axis: equal probe work per
     // shard whatever the degree skew; a shard boundary cuts a task like a piece boundary does.
@@ -369,14 +390,24 @@ template <bool kQuads>
 __global__ void __launch_bounds__(kThreads) k_support_prep(DevGraph g, unsigned long long* wpre, unsigned long long* bsum,
                                                            SupportCtl* ctl) {
     unsigned long long elems = 0;
+    unsigned long long big = 0;  // work items whose owner list is longer than kSupBigDeg (geometry choice)
     prep_items<kThreads>(g.m, [&](uint32_t t) {
         const uint32_t y = g.adj[g.stask[t]];
         const uint32_t oa = g.opos[y], len = g.opos[y + 1] - oa;
         elems += len;
-        return kQuads ? quads_of(oa, len) : len;
+        const uint32_t items = kQuads ? quads_of(oa, len) : len;
+        if (kQuads) {
+            const uint32_t x = g.sx[t];
+            if (g.opos[x + 1] - g.opos[x] > kSupBigDeg) big += items;
+        }
+        return items;
     }, wpre, bsum);
-    for (int o = 16; o > 0; o >>= 1) elems += shfl64(elems, lane_id() ^ o);
+    for (int o = 16; o > 0; o >>= 1) {
+        elems += shfl64(elems, lane_id() ^ o);
+        big += shfl64(big, lane_id() ^ o);
+    }
     if (lane_id() == 0 && elems) atomicAdd(&ctl->probes, elems);
+    if (lane_id() == 0 && big) atomicAdd(&ctl->big_work, big);
 }
 
 // triangle_count (triangle.cpp:90-116): the same task stream with no per-edge writes; each
@@ -454,15 +485,25 @@ cudaError_t launch_support(const DevGraph& g, uint32_t* s, unsigned long long* w
         return !(e && e[0] == 's');
     }();
     if (tab_form) {
-        const size_t smem = kSupSmem;
-        // per-device attribute: set on every call (contexts may sit on different devices)
-        err = cudaFuncSetAttribute(k_support_tab, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (err != cudaSuccess) return err;
-        int tb = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb, k_support_tab, kTabThreads, smem);
-        if (tb < 1) tb = 1;
-        k_support_tab<<<static_cast<unsigned>(sm_count * tb), kTabThreads, smem, st>>>(g, s, wpre, bsum, nchunks, ctl, shard,
-                                                                                    nshards);
+        static const int force = [] {
+            const char* e = std::getenv("TDG_SUP_BIG");  // diagnostic A/B: 0 / 1 forces the small / big geometry
+            return e ? std::atoi(e) : -1;
+        }();
+        // both geometries are queued; the one the graph does not want exits at once (the verdict
+        // is on the device: no host round trip). Per-device attributes: set on every call.
+        const size_t smem0 = sup_smem(kSupTab), smem1 = sup_smem(2 * kSupTab);
+        if ((err = cudaFuncSetAttribute(k_support_tab<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem0))) != cudaSuccess) return err;
+        if ((err = cudaFuncSetAttribute(k_support_tab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1))) != cudaSuccess) return err;
+        int tb0 = 0, tb1 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb0, k_support_tab<0>, kTabThreads, smem0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb1, k_support_tab<1>, 2 * kTabThreads, smem1);
+        if (tb0 < 1) tb0 = 1;
+        if (tb1 < 1) tb1 = 1;
+        k_support_tab<0><<<static_cast<unsigned>(sm_count * tb0), kTabThreads, smem0, st>>>(g, s, wpre, bsum, nchunks, ctl, shard,
+                                                                                         nshards, force);
+        k_support_tab<1><<<static_cast<unsigned>(sm_count * tb1), 2 * kTabThreads, smem1, st>>>(g, s, wpre, bsum, nchunks, ctl,
+                                                                                             shard, nshards, force);
+        (*launches)++;
     } else {
         if (nshards != 1) return cudaErrorNotSupported;  // the diagnostic search form is unsharded
         k_support<<<grid, kThreads, 0, st>>>(g, s, wpre, bsum, nchunks, ctl);

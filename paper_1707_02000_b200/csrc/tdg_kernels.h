@@ -71,7 +71,10 @@ struct SupportCtl {
     unsigned long long tab_elems;     // N+(owner) elements loaded into shared-memory tables
     unsigned long long tab_segments;  // owner segments served from a shared-memory table
     unsigned long long search_items;  // work items (16-byte list quads) binary-searched in global memory instead
-    unsigned long long hub_items;     // quads x passes of owners whose N+ exceeds one table (d+ > 3/4 TDG_SUP_TAB)
+    unsigned long long hub_items;     // quads x passes of owners whose N+ exceeds one table (d+ > 3/4 of its slots)
+    unsigned long long big_work;      // work items whose owner list exceeds TDG_SUP_TAB / 4 keys (block geometry choice)
+    unsigned long long work_items;    // all work items (16-byte list quads) of the pass
+    unsigned long long big_geometry;  // 1: the 512-thread / 8192-slot geometry ran
 };
 constexpr uint32_t kMaxChunks = 1024;  // max blocks of a prep grid (one work chunk each)
 // Requires internal edge ids (launch_internal_ids): s[m] is indexed by oriented slot.
