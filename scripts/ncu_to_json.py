@@ -53,7 +53,8 @@ for f in sorted(glob.glob(os.path.join(src, "ncu_traffic_C*.csv"))):
             k[m_] = k.get(m_, 0) + d.get(m_, 0)
     # per DECOMPOSITION: k_peel is one logical launch cut into segments (table rebuilds in
     # between); k_support_tab launches once per decomposition
-    D = max(cf.get("k_support_tab", {}).get("launches", 1), 1)
+    # (the support pass queues both block geometries; the one the graph does not want exits at once)
+    D = max(cf.get("k_support_tab", {}).get("launches", 2) // 2, 1)
     for k in cf.values():
         for m_ in list(k):
             if m_ not in ("launches", "l2_hit_pct_by_launch", "ms_by_launch"):
